@@ -1,0 +1,182 @@
+/*
+ * sbvr.h -- C-ABI of libsbvr: the SBVR (arXiv 2509.18172) hot path on NVIDIA B200 (sm_100a).
+ *
+ * The four calls follow the paper's problem statement: encode
+ * weights offline, convert activations online, and run the GEMV directly on the SBVR
+ * format without decompressing it.
+ *
+ *   sbvr_encode_weights   Section 4.2, Eq. 4-11, Algorithm 1, bit assignment
+ *   sbvr_encode_vector    Section 4.3, Eq. 12
+ *   sbvr_gemv             Section 4.4: y = W x on SBVR weights, x either fp16 or SBVR
+ *   sbvr_gemv_batched     the same for T <= 16 activation vectors sharing one weight fetch
+ *
+ * Conventions (all calls):
+ *  - Plain C types only.  "Device" pointers are CUDA global-memory pointers on the current
+ *    device; "host" pointers are CPU memory.  `stream` is a cudaStream_t passed as void*
+ *    (NULL = legacy default stream).
+ *  - Ownership: the library never allocates, frees or retains memory.  Callers query sizes
+ *    (sbvr_weights_bytes, sbvr_gemv_workspace_bytes), allocate, and pass raw pointers.
+ *  - Execution: every device call only enqueues work on `stream`; it never synchronizes the
+ *    device, and it is CUDA-graph capturable.  Arguments are validated before any launch.
+ *  - Errors: every call returns an sbvr_status.  SBVR_OK = success.  Validation failures
+ *    return SBVR_ERR_INVALID_ARG / _SHAPE / _UNSUPPORTED / _ALIGNMENT / _WORKSPACE without
+ *    enqueuing anything; a failed launch returns SBVR_ERR_CUDA.  sbvr_last_error() gives a
+ *    thread-local human-readable detail.  No C++ exception crosses this ABI.
+ *  - Determinism: no floating-point atomics; reduction orders are fixed for a given device
+ *    (SM count).  Integer outputs (planes, partials) are bit-exact.
+ *
+ * ---------------------------------------------------------------------------------------
+ * Canonical (interchange) layouts -- what tests compare against the oracle:
+ *   planes  [M][N/G][K][G/32] uint32, bit i of word w = element 32w+i of the group, LSB first
+ *   meta    s16, b16 [M][N/G] IEEE fp16 bit patterns; r_idx [M][N/G] uint8 (index into R)
+ *
+ * Device weight layout (written by sbvr_encode_weights, read by the GEMV kernels; G = 128):
+ *   Rows are cut into row tiles of 16 rows (M % 16 == 0).  Row tiles are grouped into bands
+ *   of up to 4 tiles (64 rows; the last band holds MT % 4 tiles if MT = M/16 is not a
+ *   multiple of 4).  A "tile" is (row tile rt, group g): 16 rows x 128 columns x K planes.
+ *   Tiles are stored band by band; inside a band group-major, then tile-in-band:
+ *       L(rt, g) = 4*b*NG + g*nb + (rt - 4*b),  b = rt/4, nb = min(4, MT - 4*b), NG = N/128.
+ *   Tile L occupies 256*K bytes at planes + 64*K*L words, as ceil(K/2) chunks; chunk q holds
+ *   planes 2q and 2q+1 as [lane 0..31][4 words] (the last chunk of odd K: [lane][2 words]).
+ *   Lane = 4*(row%8) + c holds, for each plane t of the chunk, word c (elements 32c..32c+31
+ *   of the group) of row (row%8) then of row (row%8)+8: word index (t%2)*2 + (row%16)/8.
+ *   This is the A-fragment order of mma.m16n8k32 (lane = 4*groupID + threadID_in_group), so
+ *   each warp-wide 16-byte load lands one plane pair of a tile directly in registers.
+ *   scale_bias[16*L + 2*(row%8) + (row%16)/8] = fp16 s (bits 0-15) | fp16 b (bits 16-31)
+ *   ratio_idx [16*L + 2*(row%8) + (row%16)/8] = uint8 index into R
+ *   ratio_pow [n_ratio][K] fp32 = r_i^t (repeated multiplication in fp64, rounded to fp32)
+ *
+ * Device activation layout (SBVR-x, written by sbvr_encode_vector):
+ *   planes [T][N/G][l][G/32] uint32 (same bit order as the weights), scales [T][N/G] fp32.
+ *   fp16-x: x is uint16_t (IEEE fp16 bits) [T][N].
+ */
+#ifndef SBVR_H_
+#define SBVR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBVR_ABI_VERSION 1
+
+typedef enum {
+  SBVR_OK = 0,
+  SBVR_ERR_INVALID_ARG = 1,  /* null pointer, out-of-range scalar */
+  SBVR_ERR_SHAPE = 2,        /* M % 16, N % G, x.N != W.N, group sizes differ, T out of range */
+  SBVR_ERR_UNSUPPORTED = 3,  /* K, l, G or config outside what this build implements */
+  SBVR_ERR_ALIGNMENT = 4,    /* device pointer not 16-byte aligned */
+  SBVR_ERR_CUDA = 5,         /* a CUDA launch or attribute query failed */
+  SBVR_ERR_WORKSPACE = 6     /* workspace missing or too small */
+} sbvr_status;
+
+typedef enum { SBVR_F32 = 0, SBVR_F16 = 1, SBVR_BF16 = 2 } sbvr_dtype;
+typedef enum { SBVR_ACT_FP16 = 0, SBVR_ACT_SBVR = 1 } sbvr_act_kind;
+
+/* GEMV algorithm selector for sbvr_gemv_ex / sbvr_debug_partials.
+ *  AUTO  : the fastest implemented kernel for the activation kind (IMMA for SBVR-x).
+ *  POPC  : the paper's formulation, CUDA-core AND + __popc + coefficient FMAs.
+ *  IMMA  : bit-sliced popcount on the int8 tensor pipe: (plane & 0x01010101<<s) x (d_j<<(7-s))
+ *          with mma.m16n8k32.u8, which counts popc(beta_t & d_j) for 16 rows x 8 planes.   */
+typedef enum { SBVR_ALGO_AUTO = 0, SBVR_ALGO_POPC = 1, SBVR_ALGO_IMMA = 2 } sbvr_algo;
+
+/* Offline encoder knobs (SURVEY §8c.3 readings A1, A4). */
+typedef struct {
+  int32_t K;             /* weight bit-planes; 1..6 supported by the encoder, 2..4 targeted */
+  int32_t group_size;    /* elements per group along N; 128 only in this build */
+  int32_t n_ratio;       /* |R|, even, 2..64 (R = two linspaces over [-1,-0.5] and [0.5,1]) */
+  int32_t n_scale;       /* |S|, 1..4096 */
+  int32_t n_bias;        /* |B|, 1..4096 */
+  double s_min_factor;   /* s_min = s_min_factor * q95(D); 2.0 = paper Eq. 10 */
+  int32_t strict;        /* 1 = fp64 search bit-identical to the oracle (only mode in this build) */
+} sbvr_encode_config;
+
+/* Encoded weights (device pointers, caller-owned; sizes from sbvr_weights_bytes). */
+typedef struct {
+  int32_t M, N, K, group_size, n_ratio;
+  uint32_t* planes;      /* device tiled layout above, 16-byte aligned */
+  uint32_t* scale_bias;  /* fp16 pair per (row, group), tile order */
+  uint8_t* ratio_idx;    /* per (row, group), tile order */
+  float* ratio_pow;      /* [n_ratio][K] */
+} sbvr_weights;
+
+/* One activation descriptor; for T vectors the buffers hold T contiguous vectors. */
+typedef struct {
+  int32_t kind;          /* sbvr_act_kind */
+  int32_t N, group_size; /* must equal the weights' N and group_size */
+  int32_t l;             /* SBVR-x activation bit-width, 2..8 (l = 8) */
+  const void* data;      /* FP16: uint16_t[T][N];  SBVR: uint32_t[T][N/G][l][G/32] */
+  const float* scales;   /* SBVR: [T][N/G]; ignored for FP16 */
+} sbvr_act;
+
+int32_t sbvr_abi_version(void);
+const char* sbvr_status_string(sbvr_status s);
+const char* sbvr_last_error(void);
+
+/* Byte sizes of the four weight buffers for an M x N matrix with K planes. */
+sbvr_status sbvr_weights_bytes(int32_t M, int32_t N, int32_t K, int32_t group_size, int32_t n_ratio,
+                               size_t* planes_bytes, size_t* scale_bias_bytes, size_t* ratio_idx_bytes,
+                               size_t* ratio_pow_bytes);
+
+/* sbvr_encode_weights -- P:150-233.  For every group of G consecutive elements of every row
+ * of W (device, row-major [M][N], dtype F32/F16/BF16), build the candidate sets of Eq. 5-11,
+ * run Algorithm 1's exhaustive MSE search over R x S x B (R outer, S middle, B inner, strict
+ * '<'), assign each element the mask of its nearest subset sum, and write planes,
+ * scale_bias, ratio_idx and ratio_pow of `out` (whose M, N, K, group_size, n_ratio must match
+ * cfg / the arguments).  group_mse (nullable, device, [M][N/G] fp64, row-major) receives each
+ * group's winning MSE.  Groups run in parallel on the GPU. */
+sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, int32_t dtype, int32_t M,
+                                int32_t N, const sbvr_weights* out, double* group_mse, void* stream);
+
+/* sbvr_encode_vector -- P:235-243, Eq. 12.  x: device fp16 bits [T][N].  Per group of G:
+ * s_x = absmax/(2^(l-1)-1) (fp32 IEEE), z = clamp(rne(x/s_x)), planes = l-bit two's
+ * complement of z (plane l-1 = sign, weight -2^(l-1) s_x).  Outputs (device):
+ * planes_out [T][N/G][l][G/32] uint32, scales_out [T][N/G] fp32.  All-zero group -> s_x = 0. */
+sbvr_status sbvr_encode_vector(const uint16_t* x, int32_t T, int32_t N, int32_t group_size, int32_t l,
+                               uint32_t* planes_out, float* scales_out, void* stream);
+
+/* Workspace for the GEMV kernels (split-row fix-up slots and counters).  The first use of a
+ * workspace requires it zeroed (sbvr_workspace_init); kernels leave it zeroed again.  One
+ * workspace must not be used by two GEMVs running concurrently on different streams. */
+sbvr_status sbvr_gemv_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* bytes);
+sbvr_status sbvr_workspace_init(void* workspace, size_t bytes, void* stream);
+
+/* sbvr_gemv -- P:245-251.  y[M] (device fp32) = W x with W in SBVR form, never decompressed.
+ * SBVR-x: y_r = sum_g s_x,g sum_t c_t sum_j alpha_j popc(beta_t & d_j), c_t = s r^t + b
+ * (alpha_j = 2^j, alpha_{l-1} = -2^(l-1)); fp16-x: y_r = sum_g sum_t c_t sum_e beta_t[e] x_e.
+ * Popcount partials are exact integers; the float part accumulates in fp32. */
+sbvr_status sbvr_gemv(const sbvr_weights* w, const sbvr_act* x, float* y, void* workspace, size_t ws_bytes,
+                      void* stream);
+
+/* sbvr_gemv_batched -- T (1..16) activation vectors in one descriptor; Y [T][M] fp32. */
+sbvr_status sbvr_gemv_batched(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
+                              size_t ws_bytes, void* stream);
+
+/* sbvr_gemv_ex -- as sbvr_gemv_batched with an explicit algorithm (sbvr_algo). */
+sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
+                         size_t ws_bytes, int32_t algo, void* stream);
+
+/* Test-only: the integer popcount partials P[m][g][t][j] = popc(beta_t & d_j) over the group,
+ * int32 [M][N/G][K][l] row-major (device), computed by the kernel `algo` (POPC or IMMA) from an
+ * SBVR-x activation (T = 1). */
+sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_t algo, int32_t* P, void* stream);
+
+/* Host-side layout transforms (host memory on both sides, no device work).  canonical planes
+ * [M][N/G][K][G/32], s16/b16/r_idx [M][N/G]  <->  device-layout images planes/scale_bias/
+ * ratio_idx (sizes as sbvr_weights_bytes).  Bit-exact inverses of each other. */
+sbvr_status sbvr_pack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_canon,
+                                const uint16_t* s16, const uint16_t* b16, const uint8_t* r_idx,
+                                uint32_t* planes_dev, uint32_t* scale_bias_dev, uint8_t* ratio_idx_dev);
+sbvr_status sbvr_unpack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_dev,
+                                  const uint32_t* scale_bias_dev, const uint8_t* ratio_idx_dev,
+                                  uint32_t* planes_canon, uint16_t* s16, uint16_t* b16, uint8_t* r_idx);
+
+/* Write w->ratio_pow (device) for w->n_ratio, w->K (used when weights arrive via pack). */
+sbvr_status sbvr_fill_ratio_table(const sbvr_weights* w, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBVR_H_ */

@@ -1,0 +1,333 @@
+"""paper_2509_18172_b200 -- SBVR (arXiv 2509.18172) hot path on B200, Python binding.
+
+This module only marshals arguments into the C-ABI of ``libsbvr.so`` (``include/sbvr.h``):
+torch tensors provide device memory and the current CUDA stream; every step of the path
+runs in the library's CUDA kernels.  There is no CPU fallback: if the shared library cannot
+be loaded the import of the first call raises.
+
+Names follow the C-ABI: ``encode_weights``, ``encode_vector``, ``gemv``, ``gemv_batched``
+(plus ``gemv_ex``, ``debug_partials``, ``pack_canonical``, ``unpack_canonical``).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import build as _build
+
+_lib = None
+
+OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_ALIGNMENT, ERR_CUDA, ERR_WORKSPACE = range(7)
+F32, F16, BF16 = 0, 1, 2
+ACT_FP16, ACT_SBVR = 0, 1
+ALGO_AUTO, ALGO_POPC, ALGO_IMMA = 0, 1, 2
+G = 128
+
+
+class SbvrError(RuntimeError):
+    def __init__(self, status: int, what: str, detail: str):
+        super().__init__(f"{what} failed: status {status} ({detail})")
+        self.status = status
+
+
+class _EncCfg(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int32), ("group_size", ctypes.c_int32), ("n_ratio", ctypes.c_int32),
+                ("n_scale", ctypes.c_int32), ("n_bias", ctypes.c_int32), ("s_min_factor", ctypes.c_double),
+                ("strict", ctypes.c_int32)]
+
+
+class _Weights(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int32), ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_size", ctypes.c_int32),
+                ("n_ratio", ctypes.c_int32), ("planes", ctypes.c_void_p), ("scale_bias", ctypes.c_void_p),
+                ("ratio_idx", ctypes.c_void_p), ("ratio_pow", ctypes.c_void_p)]
+
+
+class _Act(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("N", ctypes.c_int32), ("group_size", ctypes.c_int32),
+                ("l", ctypes.c_int32), ("data", ctypes.c_void_p), ("scales", ctypes.c_void_p)]
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def lib():
+    """Load libsbvr.so (building it in-tree with nvcc if it is missing or stale)."""
+    global _lib
+    if _lib is None:
+        if not _build.up_to_date():
+            _build.build()
+        L = ctypes.CDLL(_build.LIB)
+        P, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+        L.sbvr_abi_version.restype = i32
+        L.sbvr_status_string.restype = ctypes.c_char_p
+        L.sbvr_status_string.argtypes = [i32]
+        L.sbvr_last_error.restype = ctypes.c_char_p
+        L.sbvr_weights_bytes.argtypes = [i32, i32, i32, i32, i32, P, P, P, P]
+        L.sbvr_encode_weights.argtypes = [P, P, i32, i32, i32, P, P, P]
+        L.sbvr_encode_vector.argtypes = [P, i32, i32, i32, i32, P, P, P]
+        L.sbvr_gemv_workspace_bytes.argtypes = [P, i32, P]
+        L.sbvr_workspace_init.argtypes = [P, sz, P]
+        L.sbvr_gemv.argtypes = [P, P, P, P, sz, P]
+        L.sbvr_gemv_batched.argtypes = [P, P, i32, P, P, sz, P]
+        L.sbvr_gemv_ex.argtypes = [P, P, i32, P, P, sz, i32, P]
+        L.sbvr_debug_partials.argtypes = [P, P, i32, P, P]
+        L.sbvr_pack_canonical.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P, P]
+        L.sbvr_unpack_canonical.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P, P]
+        L.sbvr_fill_ratio_table.argtypes = [P, P]
+        for name in ("sbvr_weights_bytes", "sbvr_encode_weights", "sbvr_encode_vector", "sbvr_gemv_workspace_bytes",
+                     "sbvr_workspace_init", "sbvr_gemv", "sbvr_gemv_batched", "sbvr_gemv_ex", "sbvr_debug_partials",
+                     "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table"):
+            getattr(L, name).restype = i32
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != OK:
+        L = lib()
+        raise SbvrError(status, what, f"{L.sbvr_status_string(status).decode()}: {L.sbvr_last_error().decode()}")
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def _np_ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ------------------------------------------------------------------ weights
+@dataclass
+class SbvrWeights:
+    M: int
+    N: int
+    K: int
+    n_ratio: int
+    planes: torch.Tensor      # int32 (bit pattern of uint32), device tiled layout
+    scale_bias: torch.Tensor  # int32 (fp16 s | fp16 b << 16)
+    ratio_idx: torch.Tensor   # uint8
+    ratio_pow: torch.Tensor   # float32 [n_ratio, K]
+
+    def desc(self) -> _Weights:
+        return _Weights(self.M, self.N, self.K, G, self.n_ratio, self.planes.data_ptr(), self.scale_bias.data_ptr(),
+                        self.ratio_idx.data_ptr(), self.ratio_pow.data_ptr())
+
+    @property
+    def nbytes(self) -> int:
+        """Algorithmic bytes of the encoded weights (planes + 5 B/group metadata)."""
+        return self.planes.numel() * 4 + self.scale_bias.numel() * 4 + self.ratio_idx.numel()
+
+    def shard_rows(self, r0: int, r1: int) -> "SbvrWeights":
+        raise NotImplementedError("shard before encoding: encode each rank's row slice (see dist.py)")
+
+
+def weights_bytes(M: int, N: int, K: int, n_ratio: int = 16):
+    out = [ctypes.c_size_t() for _ in range(4)]
+    _check(lib().sbvr_weights_bytes(M, N, K, G, n_ratio, *[ctypes.byref(o) for o in out]), "sbvr_weights_bytes")
+    return tuple(o.value for o in out)
+
+
+def weights_empty(M: int, N: int, K: int, n_ratio: int = 16, device="cuda") -> SbvrWeights:
+    pb, sbb, rib, rpb = weights_bytes(M, N, K, n_ratio)
+    dev = torch.device(device)
+    return SbvrWeights(M, N, K, n_ratio, torch.empty(pb // 4, dtype=torch.int32, device=dev),
+                       torch.empty(sbb // 4, dtype=torch.int32, device=dev),
+                       torch.empty(rib + 16, dtype=torch.uint8, device=dev)[:rib],
+                       torch.empty((n_ratio, K), dtype=torch.float32, device=dev))
+
+
+_DT = {torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}
+
+
+def encode_weights(W: torch.Tensor, K: int = 4, n_ratio: int = 16, n_scale: int = 64, n_bias: int = 16,
+                   s_min_factor: float = 2.0, return_mse: bool = False, out: Optional[SbvrWeights] = None):
+    """sbvr_encode_weights: W is a CUDA [M, N] fp32/fp16/bf16 tensor."""
+    assert W.is_cuda and W.dim() == 2 and W.is_contiguous()
+    M, N = W.shape
+    w = out if out is not None else weights_empty(M, N, K, n_ratio, W.device)
+    cfg = _EncCfg(K, G, n_ratio, n_scale, n_bias, float(s_min_factor), 1)
+    mse = torch.empty((M, N // G), dtype=torch.float64, device=W.device) if return_mse else None
+    d = w.desc()
+    _check(lib().sbvr_encode_weights(ctypes.byref(cfg), _ptr(W), _DT[W.dtype], M, N, ctypes.byref(d), _ptr(mse),
+                                     _stream()), "sbvr_encode_weights")
+    return (w, mse) if return_mse else w
+
+
+# ------------------------------------------------------------------ activations
+@dataclass
+class SbvrActivation:
+    """An activation descriptor: SBVR-x (planes [T][N/G][l][4] + scales [T][N/G]) or fp16-x."""
+    kind: int
+    N: int
+    T: int
+    l: int
+    data: torch.Tensor
+    scales: Optional[torch.Tensor] = None
+
+    def desc(self) -> _Act:
+        return _Act(self.kind, self.N, G, self.l, self.data.data_ptr(),
+                    self.scales.data_ptr() if self.scales is not None else 0)
+
+
+def encode_vector(x: torch.Tensor, l: int = 8, out: Optional[SbvrActivation] = None) -> SbvrActivation:
+    """sbvr_encode_vector: x CUDA fp16 [N] or [T, N] (Eq. 12)."""
+    assert x.is_cuda and x.dtype == torch.float16 and x.is_contiguous()
+    x2 = x.view(1, -1) if x.dim() == 1 else x
+    T, N = x2.shape
+    if out is None:
+        out = SbvrActivation(ACT_SBVR, N, T, l, torch.empty(T * (N // G) * l * 4, dtype=torch.int32, device=x.device),
+                             torch.empty(T * (N // G), dtype=torch.float32, device=x.device))
+    _check(lib().sbvr_encode_vector(_ptr(x2), T, N, G, l, _ptr(out.data), _ptr(out.scales), _stream()),
+           "sbvr_encode_vector")
+    return out
+
+
+def fp16_activation(x: torch.Tensor) -> SbvrActivation:
+    assert x.is_cuda and x.dtype == torch.float16 and x.is_contiguous()
+    x2 = x.view(1, -1) if x.dim() == 1 else x
+    return SbvrActivation(ACT_FP16, x2.shape[1], x2.shape[0], 0, x2)
+
+
+# ------------------------------------------------------------------ GEMV
+class Workspace:
+    """Caller-owned GEMV workspace (zeroed once; kernels leave it zeroed)."""
+
+    def __init__(self, nbytes: int, device="cuda"):
+        self.nbytes = max(int(nbytes), 256)
+        self.buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
+
+    @staticmethod
+    def for_weights(w: SbvrWeights, T: int = 16) -> "Workspace":
+        n = ctypes.c_size_t()
+        d = w.desc()
+        _check(lib().sbvr_gemv_workspace_bytes(ctypes.byref(d), T, ctypes.byref(n)), "sbvr_gemv_workspace_bytes")
+        return Workspace(n.value, w.planes.device)
+
+
+def gemv_ex(w: SbvrWeights, x: SbvrActivation, y: Optional[torch.Tensor] = None, ws: Optional[Workspace] = None,
+            algo: int = ALGO_AUTO) -> torch.Tensor:
+    T = x.T
+    if y is None:
+        y = torch.empty((T, w.M), dtype=torch.float32, device=w.planes.device)
+    if ws is None:
+        ws = Workspace.for_weights(w, T)
+    wd, xd = w.desc(), x.desc()
+    _check(lib().sbvr_gemv_ex(ctypes.byref(wd), ctypes.byref(xd), T, _ptr(y), _ptr(ws.buf), ws.nbytes, algo,
+                              _stream()), "sbvr_gemv_ex")
+    return y
+
+
+def gemv(w: SbvrWeights, x: SbvrActivation, y: Optional[torch.Tensor] = None,
+         ws: Optional[Workspace] = None) -> torch.Tensor:
+    """sbvr_gemv: y[M] = W x on the SBVR weights, x SBVR-encoded or fp16."""
+    assert x.T == 1
+    if y is None:
+        y = torch.empty(w.M, dtype=torch.float32, device=w.planes.device)
+    if ws is None:
+        ws = Workspace.for_weights(w, 1)
+    wd, xd = w.desc(), x.desc()
+    _check(lib().sbvr_gemv(ctypes.byref(wd), ctypes.byref(xd), _ptr(y), _ptr(ws.buf), ws.nbytes, _stream()),
+           "sbvr_gemv")
+    return y
+
+
+def gemv_batched(w: SbvrWeights, X: SbvrActivation, Y: Optional[torch.Tensor] = None,
+                 ws: Optional[Workspace] = None) -> torch.Tensor:
+    """sbvr_gemv_batched: Y[T, M] for T <= 16 vectors sharing one weight fetch."""
+    if Y is None:
+        Y = torch.empty((X.T, w.M), dtype=torch.float32, device=w.planes.device)
+    if ws is None:
+        ws = Workspace.for_weights(w, X.T)
+    wd, xd = w.desc(), X.desc()
+    _check(lib().sbvr_gemv_batched(ctypes.byref(wd), ctypes.byref(xd), X.T, _ptr(Y), _ptr(ws.buf), ws.nbytes,
+                                   _stream()), "sbvr_gemv_batched")
+    return Y
+
+
+def debug_partials(w: SbvrWeights, x: SbvrActivation, algo: int = ALGO_IMMA) -> torch.Tensor:
+    P = torch.full((w.M, w.N // G, w.K, x.l), -1, dtype=torch.int32, device=w.planes.device)
+    wd, xd = w.desc(), x.desc()
+    _check(lib().sbvr_debug_partials(ctypes.byref(wd), ctypes.byref(xd), algo, _ptr(P), _stream()),
+           "sbvr_debug_partials")
+    return P
+
+
+# ------------------------------------------------------------------ host layout transforms
+def pack_canonical(planes_canon: np.ndarray, s16: np.ndarray, b16: np.ndarray, r_idx: np.ndarray, n_ratio: int = 16,
+                   device="cuda") -> SbvrWeights:
+    """Canonical [M][N/G][K][4] planes + meta -> device SbvrWeights (host transform, then upload)."""
+    M, NG, K, _ = planes_canon.shape
+    N = NG * G
+    pb, sbb, rib, _ = weights_bytes(M, N, K, n_ratio)
+    pd = np.zeros(pb // 4, np.uint32)
+    sbd = np.zeros(sbb // 4, np.uint32)
+    rid = np.zeros(rib, np.uint8)
+    pc = np.ascontiguousarray(planes_canon, np.uint32)
+    s16 = np.ascontiguousarray(s16, np.uint16)
+    b16 = np.ascontiguousarray(b16, np.uint16)
+    r_idx = np.ascontiguousarray(r_idx, np.uint8)
+    _check(lib().sbvr_pack_canonical(M, N, K, G, _np_ptr(pc), _np_ptr(s16), _np_ptr(b16), _np_ptr(r_idx), _np_ptr(pd),
+                                     _np_ptr(sbd), _np_ptr(rid)), "sbvr_pack_canonical")
+    w = weights_empty(M, N, K, n_ratio, device)
+    w.planes.copy_(torch.from_numpy(pd.view(np.int32)))
+    w.scale_bias.copy_(torch.from_numpy(sbd.view(np.int32)))
+    w.ratio_idx.copy_(torch.from_numpy(rid))
+    d = w.desc()
+    _check(lib().sbvr_fill_ratio_table(ctypes.byref(d), _stream()), "sbvr_fill_ratio_table")
+    return w
+
+
+def unpack_canonical(w: SbvrWeights):
+    """Device SbvrWeights -> canonical numpy (planes [M][N/G][K][4] uint32, s16, b16, r_idx [M][N/G])."""
+    NG = w.N // G
+    pd = w.planes.cpu().numpy().view(np.uint32).copy()
+    sbd = w.scale_bias.cpu().numpy().view(np.uint32).copy()
+    rid = w.ratio_idx.cpu().numpy().copy()
+    return unpack_host(w.M, w.N, w.K, pd, sbd, rid)
+
+
+def unpack_host(M: int, N: int, K: int, pd: np.ndarray, sbd: np.ndarray, rid: np.ndarray):
+    NG = N // G
+    pc = np.zeros((M, NG, K, 4), np.uint32)
+    s16 = np.zeros((M, NG), np.uint16)
+    b16 = np.zeros((M, NG), np.uint16)
+    ri = np.zeros((M, NG), np.uint8)
+    pd = np.ascontiguousarray(pd, np.uint32)
+    sbd = np.ascontiguousarray(sbd, np.uint32)
+    rid = np.ascontiguousarray(rid, np.uint8)
+    _check(lib().sbvr_unpack_canonical(M, N, K, G, _np_ptr(pd), _np_ptr(sbd), _np_ptr(rid), _np_ptr(pc), _np_ptr(s16),
+                                       _np_ptr(b16), _np_ptr(ri)), "sbvr_unpack_canonical")
+    return pc, s16, b16, ri
+
+
+def pack_host(planes_canon, s16, b16, r_idx):
+    """Canonical -> device-layout images on the host (numpy); used by layout tests."""
+    M, NG, K, _ = planes_canon.shape
+    N = NG * G
+    pb, sbb, rib, _ = weights_bytes(M, N, K)
+    pd = np.zeros(pb // 4, np.uint32)
+    sbd = np.zeros(sbb // 4, np.uint32)
+    rid = np.zeros(rib, np.uint8)
+    _check(lib().sbvr_pack_canonical(M, N, K, G, _np_ptr(np.ascontiguousarray(planes_canon, np.uint32)),
+                                     _np_ptr(np.ascontiguousarray(s16, np.uint16)),
+                                     _np_ptr(np.ascontiguousarray(b16, np.uint16)),
+                                     _np_ptr(np.ascontiguousarray(r_idx, np.uint8)), _np_ptr(pd), _np_ptr(sbd),
+                                     _np_ptr(rid)), "sbvr_pack_canonical")
+    return pd, sbd, rid
+
+
+def algorithmic_bytes(M: int, N: int, K: int, act: str = "sbvr", l: int = 8, T: int = 1) -> int:
+    """B = M N K/8 + 5 M N/G + x + 4 M (x = 2N fp16, or N l/8 + 4 N/G SBVR), per token for x/y."""
+    x = 2 * N if act == "fp16" else N * l // 8 + 4 * (N // G)
+    return M * N * K // 8 + 5 * M * (N // G) + T * (x + 4 * M)

@@ -1,0 +1,251 @@
+// abi.cu -- extern "C" entry points of libsbvr (include/sbvr.h): argument validation,
+// size queries, host-side layout transforms and dispatch to the kernels.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "sbvr_internal.cuh"
+
+namespace sbvr {
+
+static thread_local char g_err[512] = "";
+
+sbvr_status set_error(sbvr_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+sbvr_status check_launch(const char* what) {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_error(SBVR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  }
+  return SBVR_OK;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static sbvr_status check_weights(const sbvr_weights* w) {
+  if (!w) return set_error(SBVR_ERR_INVALID_ARG, "weights descriptor is NULL");
+  if (!w->planes || !w->scale_bias || !w->ratio_idx || !w->ratio_pow)
+    return set_error(SBVR_ERR_INVALID_ARG, "weights buffer pointer is NULL");
+  if (w->group_size != kG) return set_error(SBVR_ERR_UNSUPPORTED, "group_size %d (only 128)", w->group_size);
+  if (w->K < 1 || w->K > kMaxK) return set_error(SBVR_ERR_UNSUPPORTED, "K=%d outside 1..8", w->K);
+  if (w->n_ratio < 2 || w->n_ratio > 64 || (w->n_ratio & 1))
+    return set_error(SBVR_ERR_INVALID_ARG, "n_ratio=%d must be even in 2..64", w->n_ratio);
+  if (w->M <= 0 || w->N <= 0) return set_error(SBVR_ERR_SHAPE, "M=%d N=%d must be positive", w->M, w->N);
+  if (w->M % kTileRows) return set_error(SBVR_ERR_SHAPE, "M=%d not a multiple of 16", w->M);
+  if (w->N % kG) return set_error(SBVR_ERR_SHAPE, "N=%d not a multiple of group_size 128", w->N);
+  if (!aligned16(w->planes) || !aligned16(w->scale_bias) || !aligned16(w->ratio_pow))
+    return set_error(SBVR_ERR_ALIGNMENT, "weights buffers must be 16-byte aligned");
+  return SBVR_OK;
+}
+
+static sbvr_status check_act(const sbvr_weights* w, const sbvr_act* x, int T) {
+  if (!x || !x->data) return set_error(SBVR_ERR_INVALID_ARG, "activation descriptor/data is NULL");
+  if (T < 1 || T > kMaxT) return set_error(SBVR_ERR_SHAPE, "T=%d outside 1..16", T);
+  if (x->N != w->N) return set_error(SBVR_ERR_SHAPE, "x.N=%d != W.N=%d", x->N, w->N);
+  if (x->group_size != w->group_size)
+    return set_error(SBVR_ERR_SHAPE, "x.group_size=%d != W.group_size=%d", x->group_size, w->group_size);
+  if (x->kind == SBVR_ACT_SBVR) {
+    if (!x->scales) return set_error(SBVR_ERR_INVALID_ARG, "SBVR activation scales are NULL");
+    if (x->l < 2 || x->l > 8) return set_error(SBVR_ERR_UNSUPPORTED, "l=%d outside 2..8", x->l);
+    if (!aligned16(x->data)) return set_error(SBVR_ERR_ALIGNMENT, "activation planes must be 16-byte aligned");
+  } else if (x->kind == SBVR_ACT_FP16) {
+    if (!aligned16(x->data)) return set_error(SBVR_ERR_ALIGNMENT, "fp16 activation must be 16-byte aligned");
+  } else {
+    return set_error(SBVR_ERR_INVALID_ARG, "unknown activation kind %d", x->kind);
+  }
+  return SBVR_OK;
+}
+
+}  // namespace sbvr
+
+using namespace sbvr;
+
+extern "C" {
+
+int32_t sbvr_abi_version(void) { return SBVR_ABI_VERSION; }
+
+const char* sbvr_status_string(sbvr_status s) {
+  switch (s) {
+    case SBVR_OK: return "SBVR_OK";
+    case SBVR_ERR_INVALID_ARG: return "SBVR_ERR_INVALID_ARG";
+    case SBVR_ERR_SHAPE: return "SBVR_ERR_SHAPE";
+    case SBVR_ERR_UNSUPPORTED: return "SBVR_ERR_UNSUPPORTED";
+    case SBVR_ERR_ALIGNMENT: return "SBVR_ERR_ALIGNMENT";
+    case SBVR_ERR_CUDA: return "SBVR_ERR_CUDA";
+    case SBVR_ERR_WORKSPACE: return "SBVR_ERR_WORKSPACE";
+  }
+  return "SBVR_UNKNOWN_STATUS";
+}
+
+const char* sbvr_last_error(void) { return g_err; }
+
+sbvr_status sbvr_weights_bytes(int32_t M, int32_t N, int32_t K, int32_t group_size, int32_t n_ratio,
+                               size_t* planes_bytes, size_t* scale_bias_bytes, size_t* ratio_idx_bytes,
+                               size_t* ratio_pow_bytes) {
+  if (!planes_bytes || !scale_bias_bytes || !ratio_idx_bytes || !ratio_pow_bytes)
+    return set_error(SBVR_ERR_INVALID_ARG, "output pointer is NULL");
+  if (group_size != kG) return set_error(SBVR_ERR_UNSUPPORTED, "group_size %d (only 128)", group_size);
+  if (K < 1 || K > kMaxK) return set_error(SBVR_ERR_UNSUPPORTED, "K=%d outside 1..8", K);
+  if (M <= 0 || N <= 0 || M % kTileRows || N % kG)
+    return set_error(SBVR_ERR_SHAPE, "M=%d must be a positive multiple of 16, N=%d of 128", M, N);
+  if (n_ratio < 2 || n_ratio > 64 || (n_ratio & 1)) return set_error(SBVR_ERR_INVALID_ARG, "bad n_ratio %d", n_ratio);
+  size_t groups = (size_t)M * (N / kG);
+  *planes_bytes = groups * (size_t)K * kWPG * 4;
+  *scale_bias_bytes = groups * 4;
+  *ratio_idx_bytes = groups;
+  *ratio_pow_bytes = (size_t)n_ratio * K * 4;
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, int32_t dtype, int32_t M, int32_t N,
+                                const sbvr_weights* out, double* group_mse, void* stream) {
+  if (!cfg || !W || !out) return set_error(SBVR_ERR_INVALID_ARG, "cfg/W/out is NULL");
+  if (dtype != SBVR_F32 && dtype != SBVR_F16 && dtype != SBVR_BF16)
+    return set_error(SBVR_ERR_INVALID_ARG, "unknown dtype %d", dtype);
+  if (cfg->K < 1 || cfg->K > 6) return set_error(SBVR_ERR_UNSUPPORTED, "encoder K=%d outside 1..6", cfg->K);
+  if (cfg->group_size != kG) return set_error(SBVR_ERR_UNSUPPORTED, "group_size %d (only 128)", cfg->group_size);
+  if (cfg->n_ratio < 2 || cfg->n_ratio > 64 || (cfg->n_ratio & 1))
+    return set_error(SBVR_ERR_INVALID_ARG, "n_ratio=%d must be even in 2..64", cfg->n_ratio);
+  if (cfg->n_scale < 1 || cfg->n_scale > 4096 || cfg->n_bias < 1 || cfg->n_bias > 4096)
+    return set_error(SBVR_ERR_INVALID_ARG, "n_scale/n_bias outside 1..4096");
+  if (!cfg->strict) return set_error(SBVR_ERR_UNSUPPORTED, "only strict (fp64, oracle-exact) encoding is built");
+  if (out->M != M || out->N != N || out->K != cfg->K || out->group_size != cfg->group_size ||
+      out->n_ratio != cfg->n_ratio)
+    return set_error(SBVR_ERR_SHAPE, "output descriptor does not match M/N/K/group_size/n_ratio");
+  sbvr_status s = check_weights(out);
+  if (s != SBVR_OK) return s;
+  return launch_encode_weights(cfg, W, dtype, M, N, out, group_mse, (cudaStream_t)stream);
+}
+
+sbvr_status sbvr_encode_vector(const uint16_t* x, int32_t T, int32_t N, int32_t group_size, int32_t l,
+                               uint32_t* planes_out, float* scales_out, void* stream) {
+  if (!x || !planes_out || !scales_out) return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  if (group_size != kG) return set_error(SBVR_ERR_UNSUPPORTED, "group_size %d (only 128)", group_size);
+  if (l < 2 || l > 8) return set_error(SBVR_ERR_UNSUPPORTED, "l=%d outside 2..8", l);
+  if (T < 1 || N <= 0 || N % kG) return set_error(SBVR_ERR_SHAPE, "T=%d N=%d", T, N);
+  return launch_encode_vector(x, T, N, l, planes_out, scales_out, (cudaStream_t)stream);
+}
+
+sbvr_status sbvr_gemv_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* bytes) {
+  if (!w || !bytes) return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  if (T < 1 || T > kMaxT) return set_error(SBVR_ERR_SHAPE, "T=%d outside 1..16", T);
+  if (w->M <= 0 || w->N <= 0 || w->M % kTileRows || w->N % kG)
+    return set_error(SBVR_ERR_SHAPE, "bad M/N %d/%d", w->M, w->N);
+  *bytes = imma_workspace_bytes(w, T);
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_workspace_init(void* workspace, size_t bytes, void* stream) {
+  if (!workspace && bytes) return set_error(SBVR_ERR_INVALID_ARG, "workspace is NULL");
+  if (bytes == 0) return SBVR_OK;
+  cudaError_t e = cudaMemsetAsync(workspace, 0, bytes, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
+                         size_t ws_bytes, int32_t algo, void* stream) {
+  sbvr_status s = check_weights(w);
+  if (s != SBVR_OK) return s;
+  s = check_act(w, X, T);
+  if (s != SBVR_OK) return s;
+  if (!Y) return set_error(SBVR_ERR_INVALID_ARG, "Y is NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (X->kind == SBVR_ACT_FP16) {
+    if (algo == SBVR_ALGO_IMMA) return set_error(SBVR_ERR_UNSUPPORTED, "IMMA fp16-x kernel not built");
+    return launch_gemv_fp16x(w, X, T, Y, st);
+  }
+  if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, X, T, Y, nullptr, st);
+  if (algo != SBVR_ALGO_AUTO && algo != SBVR_ALGO_IMMA) return set_error(SBVR_ERR_INVALID_ARG, "bad algo %d", algo);
+  size_t need = imma_workspace_bytes(w, T);
+  if (need && (!workspace || ws_bytes < need))
+    return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+  return launch_gemv_imma(w, X, T, Y, workspace, ws_bytes, nullptr, st);
+}
+
+sbvr_status sbvr_gemv(const sbvr_weights* w, const sbvr_act* x, float* y, void* workspace, size_t ws_bytes,
+                      void* stream) {
+  return sbvr_gemv_ex(w, x, 1, y, workspace, ws_bytes, SBVR_ALGO_AUTO, stream);
+}
+
+sbvr_status sbvr_gemv_batched(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
+                              size_t ws_bytes, void* stream) {
+  return sbvr_gemv_ex(w, X, T, Y, workspace, ws_bytes, SBVR_ALGO_AUTO, stream);
+}
+
+sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_t algo, int32_t* P, void* stream) {
+  sbvr_status s = check_weights(w);
+  if (s != SBVR_OK) return s;
+  s = check_act(w, x, 1);
+  if (s != SBVR_OK) return s;
+  if (!P) return set_error(SBVR_ERR_INVALID_ARG, "P is NULL");
+  if (x->kind != SBVR_ACT_SBVR) return set_error(SBVR_ERR_INVALID_ARG, "partials need an SBVR activation");
+  if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, x, 1, nullptr, P, (cudaStream_t)stream);
+  if (algo == SBVR_ALGO_IMMA || algo == SBVR_ALGO_AUTO)
+    return launch_gemv_imma(w, x, 1, nullptr, nullptr, 0, P, (cudaStream_t)stream);
+  return set_error(SBVR_ERR_INVALID_ARG, "bad algo %d", algo);
+}
+
+static sbvr_status check_pack_args(int32_t M, int32_t N, int32_t K, int32_t G) {
+  if (G != kG) return set_error(SBVR_ERR_UNSUPPORTED, "group_size %d (only 128)", G);
+  if (K < 1 || K > kMaxK) return set_error(SBVR_ERR_UNSUPPORTED, "K=%d", K);
+  if (M <= 0 || N <= 0 || M % kTileRows || N % kG) return set_error(SBVR_ERR_SHAPE, "M=%d N=%d", M, N);
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_pack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_canon,
+                                const uint16_t* s16, const uint16_t* b16, const uint8_t* r_idx, uint32_t* planes_dev,
+                                uint32_t* scale_bias_dev, uint8_t* ratio_idx_dev) {
+  sbvr_status s = check_pack_args(M, N, K, group_size);
+  if (s != SBVR_OK) return s;
+  if (!planes_canon || !s16 || !b16 || !r_idx || !planes_dev || !scale_bias_dev || !ratio_idx_dev)
+    return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  Layout Lo(M, N, K);
+  for (int r = 0; r < M; ++r)
+    for (int g = 0; g < Lo.NG; ++g) {
+      long q = (long)r * Lo.NG + g;
+      for (int t = 0; t < K; ++t)
+        for (int c = 0; c < kWPG; ++c) planes_dev[Lo.plane_word(r, g, t, c)] = planes_canon[(q * K + t) * kWPG + c];
+      long m = Lo.meta(r, g);
+      scale_bias_dev[m] = (uint32_t)s16[q] | ((uint32_t)b16[q] << 16);
+      ratio_idx_dev[m] = r_idx[q];
+    }
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_unpack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_dev,
+                                  const uint32_t* scale_bias_dev, const uint8_t* ratio_idx_dev,
+                                  uint32_t* planes_canon, uint16_t* s16, uint16_t* b16, uint8_t* r_idx) {
+  sbvr_status s = check_pack_args(M, N, K, group_size);
+  if (s != SBVR_OK) return s;
+  if (!planes_canon || !s16 || !b16 || !r_idx || !planes_dev || !scale_bias_dev || !ratio_idx_dev)
+    return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  Layout Lo(M, N, K);
+  for (int r = 0; r < M; ++r)
+    for (int g = 0; g < Lo.NG; ++g) {
+      long q = (long)r * Lo.NG + g;
+      for (int t = 0; t < K; ++t)
+        for (int c = 0; c < kWPG; ++c) planes_canon[(q * K + t) * kWPG + c] = planes_dev[Lo.plane_word(r, g, t, c)];
+      long m = Lo.meta(r, g);
+      s16[q] = (uint16_t)(scale_bias_dev[m] & 0xffffu);
+      b16[q] = (uint16_t)(scale_bias_dev[m] >> 16);
+      r_idx[q] = ratio_idx_dev[m];
+    }
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_fill_ratio_table(const sbvr_weights* w, void* stream) {
+  if (!w || !w->ratio_pow) return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  if (w->K < 1 || w->K > kMaxK) return set_error(SBVR_ERR_UNSUPPORTED, "K=%d", w->K);
+  if (w->n_ratio < 2 || w->n_ratio > 64 || (w->n_ratio & 1)) return set_error(SBVR_ERR_INVALID_ARG, "n_ratio");
+  return launch_ratio_table(w->ratio_pow, w->n_ratio, w->K, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// encode_vector.cu -- online activation conversion, §4.3, Eq. 12.
+//
+// One warp per activation group of 128 elements.  Lane L holds elements L, 32+L, 64+L, 96+L,
+// so one __ballot_sync per (plane j, word c) produces word c of bit-plane j directly:
+//   absmax (warp max-reduce, exact) -> s_x = absmax / (2^(l-1)-1)  (IEEE fp32 divide, reading A10)
+//   z = clamp(rne(x / s_x))  (cvt.rni, reading A12) -> planes = l-bit two's complement of z
+// Output: planes [T][N/G][l][4] (lane 4j+c stores word (j, c): one coalesced 128-byte store),
+// scales [T][N/G].  Memory-bound: 2N bytes in, (l/8 + 4/G) N bytes out.
+#include "sbvr_internal.cuh"
+
+namespace sbvr {
+
+__global__ void __launch_bounds__(256) encode_vector_kernel(const uint16_t* __restrict__ x, int total_groups, int l,
+                                                            uint32_t* __restrict__ planes,
+                                                            float* __restrict__ scales) {
+  const int lane = threadIdx.x & 31;
+  const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // group index over [T][N/G]
+  if (q >= total_groups) return;
+  const uint16_t* xg = x + (size_t)q * kG;                      // groups are contiguous in [T][N]
+  float v[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) v[c] = __half2float(__ushort_as_half(__ldg(xg + 32 * c + lane)));
+  float a = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+  const int zmax = (1 << (l - 1)) - 1;
+  const float sx = (a != 0.0f) ? __fdiv_rn(a, (float)zmax) : 0.0f;
+  const uint32_t lmask = (1u << l) - 1u;
+  uint32_t mine = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    int z = 0;
+    if (sx != 0.0f) {
+      z = __float2int_rn(__fdiv_rn(v[c], sx));
+      z = min(max(z, -zmax), zmax);
+    }
+    const uint32_t u = (uint32_t)z & lmask;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t word = __ballot_sync(0xffffffffu, (u >> j) & 1u);
+      if (lane == 4 * j + c) mine = word;
+    }
+  }
+  if (lane < 4 * l) planes[(size_t)q * 4 * l + lane] = mine;
+  if (lane == 0) scales[q] = sx;
+}
+
+sbvr_status launch_encode_vector(const uint16_t* x, int T, int N, int l, uint32_t* planes, float* scales,
+                                 cudaStream_t st) {
+  const int groups = T * (N / kG);
+  const int blocks = (groups * 32 + 255) / 256;
+  encode_vector_kernel<<<blocks, 256, 0, st>>>(x, groups, l, planes, scales);
+  return check_launch("encode_vector_kernel");
+}
+
+}  // namespace sbvr

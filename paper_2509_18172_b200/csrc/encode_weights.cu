@@ -1,0 +1,279 @@
+// encode_weights.cu -- offline SBVR weight encoding, §4.2, strict fp64.
+//
+// One CTA per weight group (groups are independent, "grouping facilitates parallelism
+// during the encoding step"):
+//   1. load the 128 values as fp64 (exact from fp32/fp16/bf16), bitonic-sort a copy in smem;
+//      thread 0 derives q95 (linear interpolation, reading A6), min, max and the mean
+//      (sequential sum in element order) -> s_min, s_max, s_gran, b_max, b_gran (Eq. 8-11);
+//   2. S (Eq. 6) and B (Eq. 7) candidates rounded to fp16 (reading A15), R as two linspaces
+//      over [-1,-0.5] and [0.5,1] (reading A3);
+//   3. Algorithm 1: thread t scans entries e = t, t+256, ... (R outer, S middle,
+//      B inner): c = s r^t + b (Eq. 4), 2^K subset sums, per element the distance to the
+//      nearest sum (min over all sums), SSE in element order, mse = SSE/128; strict '<' keeps
+//      the first best; a CTA arg-min (mse, then entry index) equals the sequential scan;
+//   4. P:231 bit assignment for the winner (ties: smaller value, then smaller mask, reading A8),
+//      __ballot_sync packs each 32-element word of each plane; write planes / meta / mse.
+// Every fp64 operation is an explicit _rn intrinsic in the order the paper's formulas are
+// written, so the result is bit-identical to any IEEE fp64 evaluation in that order.
+#include <cfloat>
+
+#include "sbvr_internal.cuh"
+
+namespace sbvr {
+
+__device__ __forceinline__ uint16_t f64_to_f16_bits(double x) {
+  unsigned short h;
+  asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h) : "d"(x));
+  return h;
+}
+__device__ __forceinline__ double f16_bits_to_f64(uint16_t h) {
+  float f;
+  asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h));
+  return (double)f;
+}
+
+__device__ __forceinline__ double ratio_value(int i, int n_ratio) {
+  const int half = n_ratio / 2;
+  const int part = i / half, ii = i % half;
+  const double a = part ? 0.5 : -1.0;
+  const double b = part ? 1.0 : -0.5;
+  if (half == 1) return a;
+  if (ii == half - 1) return b;
+  return __dadd_rn(__dmul_rn((double)ii, __ddiv_rn(__dsub_rn(b, a), (double)(half - 1))), a);
+}
+
+__device__ __forceinline__ double load_w(const void* W, int dtype, size_t idx) {
+  if (dtype == SBVR_F32) return (double)__ldg(reinterpret_cast<const float*>(W) + idx);
+  const unsigned short u = __ldg(reinterpret_cast<const unsigned short*>(W) + idx);
+  if (dtype == SBVR_F16) return (double)__half2float(__ushort_as_half(u));
+  return (double)__uint_as_float(((uint32_t)u) << 16);  // bf16
+}
+
+struct EncParams {
+  const void* W;
+  int dtype, M, N;
+  int n_ratio, n_scale, n_bias;
+  double s_min_factor;
+  uint32_t* planes;
+  uint32_t* scale_bias;
+  uint8_t* ratio_idx;
+  double* group_mse;
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) encode_weights_kernel(EncParams p) {
+  constexpr int NPTS = 1 << K;
+  extern __shared__ double smem[];
+  double* X = smem;                  // [128] group values (element order)
+  double* Xs = X + kG;               // [128] sorted copy
+  double* R = Xs + kG;               // [n_ratio]
+  double* S = R + 64;                // [n_scale]
+  double* B = S + p.n_scale;         // [n_bias]
+  __shared__ double s_scal[4];       // s_min, s_gran, b_min, b_gran
+  __shared__ double red_mse[8];
+  __shared__ int red_e[8];
+  __shared__ int win_e;
+  __shared__ double win_mse;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Layout Lo(p.M, p.N, K);
+  const long n_groups = (long)p.M * Lo.NG;
+  const int E = p.n_ratio * p.n_scale * p.n_bias;
+
+  for (long q = blockIdx.x; q < n_groups; q += gridDim.x) {
+    const int row = (int)(q / Lo.NG), g = (int)(q % Lo.NG);
+    if (tid < kG) {
+      const double v = load_w(p.W, p.dtype, (size_t)row * p.N + (size_t)g * kG + tid);
+      X[tid] = v;
+      Xs[tid] = v;
+    }
+    for (int i = tid; i < p.n_ratio; i += blockDim.x) R[i] = ratio_value(i, p.n_ratio);
+    __syncthreads();
+    // bitonic sort of Xs (ascending); any correct sort yields the same array
+    for (int k2 = 2; k2 <= kG; k2 <<= 1) {
+      for (int j2 = k2 >> 1; j2 > 0; j2 >>= 1) {
+        if (tid < kG) {
+          const int ixj = tid ^ j2;
+          if (ixj > tid) {
+            const double a = Xs[tid], b = Xs[ixj];
+            const bool up = ((tid & k2) == 0);
+            if ((a > b) == up) { Xs[tid] = b; Xs[ixj] = a; }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (tid == 0) {
+      // O-W1 statistics
+      const double h = __dmul_rn(0.95, (double)(kG - 1));
+      const int f = (int)floor(h);
+      const double frac = __dsub_rn(h, (double)f);
+      const double q95 = (f + 1 < kG) ? __dadd_rn(Xs[f], __dmul_rn(frac, __dsub_rn(Xs[f + 1], Xs[f]))) : Xs[f];
+      const double mn = Xs[0], mx = Xs[kG - 1];
+      double sum = 0.0;
+      for (int e = 0; e < kG; ++e) sum = __dadd_rn(sum, X[e]);
+      const double mean = __ddiv_rn(sum, (double)kG);
+      // O-W2 candidate-set parameters (Eq. 8-11)
+      const double s_min = __dmul_rn(p.s_min_factor, q95);
+      double s_max = __dmul_rn(1.1, __dsub_rn(mx, mn));
+      if (s_max <= s_min) s_max = __dmul_rn(1.01, s_min);
+      const double s_gran = __ddiv_rn(__dsub_rn(s_max, s_min), (double)p.n_scale);
+      const double b_max = __ddiv_rn(__dmul_rn(2.0, fabs(mean)), (double)K);
+      const double b_min = -b_max;
+      const double b_gran = __ddiv_rn(__dsub_rn(b_max, b_min), (double)p.n_bias);
+      s_scal[0] = s_min; s_scal[1] = s_gran; s_scal[2] = b_min; s_scal[3] = b_gran;
+    }
+    __syncthreads();
+    for (int j = tid; j < p.n_scale; j += blockDim.x)
+      S[j] = f16_bits_to_f64(f64_to_f16_bits(__dadd_rn(s_scal[0], __dmul_rn((double)(j + 1), s_scal[1]))));
+    for (int k = tid; k < p.n_bias; k += blockDim.x)
+      B[k] = f16_bits_to_f64(f64_to_f16_bits(__dadd_rn(s_scal[2], __dmul_rn((double)k, s_scal[3]))));
+    __syncthreads();
+
+    // ---- Algorithm 1: exhaustive search, entries strided over threads
+    double best = DBL_MAX;
+    int best_e = 0x7fffffff;
+    bool have = false;
+    const int SB = p.n_scale * p.n_bias;
+    for (int e = tid; e < E; e += blockDim.x) {
+      const int i = e / SB, rem = e - i * SB, j = rem / p.n_bias, k = rem - j * p.n_bias;
+      const double r = R[i], s = S[j], b = B[k];
+      double c[K];
+      double pw = 1.0;
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        c[t] = __dadd_rn(__dmul_rn(s, pw), b);
+        pw = __dmul_rn(pw, r);
+      }
+      double v[NPTS];
+#pragma unroll
+      for (int m = 0; m < NPTS; ++m) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < K; ++t)
+          if ((m >> t) & 1) acc = __dadd_rn(acc, c[t]);
+        v[m] = acc;
+      }
+      double sse = 0.0;
+#pragma unroll 2
+      for (int el = 0; el < kG; ++el) {
+        const double x = X[el];
+        double d = fabs(__dsub_rn(x, v[0]));
+#pragma unroll
+        for (int m = 1; m < NPTS; ++m) d = fmin(d, fabs(__dsub_rn(x, v[m])));
+        sse = __dadd_rn(sse, __dmul_rn(d, d));
+      }
+      const double mse = __ddiv_rn(sse, (double)kG);
+      if (!have || mse < best) { best = mse; best_e = e; have = true; }
+    }
+    // CTA arg-min: smaller mse, then smaller entry index (== the sequential strict '<' scan)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double om = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
+      if (om < best || (om == best && oe < best_e)) { best = om; best_e = oe; }
+    }
+    if (lane == 0) { red_mse[warp] = best; red_e[warp] = best_e; }
+    __syncthreads();
+    if (tid == 0) {
+      double bm = red_mse[0];
+      int be = red_e[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (red_mse[w] < bm || (red_mse[w] == bm && red_e[w] < be)) { bm = red_mse[w]; be = red_e[w]; }
+      win_e = be;
+      win_mse = bm;
+    }
+    __syncthreads();
+
+    // ---- P:231 bit assignment for the winning entry
+    const int we = win_e;
+    const int wi = we / SB, wrem = we - wi * SB, wj = wrem / p.n_bias, wk = wrem - wj * p.n_bias;
+    if (tid < kG) {
+      double c[K];
+      double pw = 1.0;
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        c[t] = __dadd_rn(__dmul_rn(S[wj], pw), B[wk]);
+        pw = __dmul_rn(pw, R[wi]);
+      }
+      const double x = X[tid];
+      int bm = 0;
+      double bd = 0.0, bv = 0.0;
+#pragma unroll
+      for (int m = 0; m < NPTS; ++m) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < K; ++t)
+          if ((m >> t) & 1) acc = __dadd_rn(acc, c[t]);
+        const double d = fabs(__dsub_rn(x, acc));
+        if (m == 0 || d < bd || (d == bd && acc < bv)) { bd = d; bv = acc; bm = m; }
+      }
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        const uint32_t word = __ballot_sync(0xffffffffu, (bm >> t) & 1);
+        if (lane == t) p.planes[Lo.plane_word(row, g, t, warp)] = word;
+      }
+    }
+    if (tid == 0) {
+      const long m = Lo.meta(row, g);
+      p.scale_bias[m] = (uint32_t)f64_to_f16_bits(S[wj]) | ((uint32_t)f64_to_f16_bits(B[wk]) << 16);
+      p.ratio_idx[m] = (uint8_t)wi;
+      if (p.group_mse) p.group_mse[q] = win_mse;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void ratio_table_kernel(float* out, int n_ratio, int K) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_ratio) return;
+  const double r = ratio_value(i, n_ratio);
+  double pw = 1.0;
+  for (int t = 0; t < K; ++t) {
+    out[i * K + t] = __double2float_rn(pw);
+    pw = __dmul_rn(pw, r);
+  }
+}
+
+sbvr_status launch_ratio_table(float* ratio_pow, int n_ratio, int K, cudaStream_t st) {
+  ratio_table_kernel<<<1, 64, 0, st>>>(ratio_pow, n_ratio, K);
+  return check_launch("ratio_table_kernel");
+}
+
+template <int K>
+static sbvr_status launch_k(const EncParams& p, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (2 * kG + 64 + p.n_scale + p.n_bias);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(encode_weights_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(e));
+  }
+  const long groups = (long)p.M * (p.N / kG);
+  const int grid = (int)(groups < (1L << 30) ? groups : (1L << 30));
+  encode_weights_kernel<K><<<grid, 256, smem, st>>>(p);
+  return check_launch("encode_weights_kernel");
+}
+
+sbvr_status launch_encode_weights(const sbvr_encode_config* cfg, const void* W, int dtype, int M, int N,
+                                  const sbvr_weights* out, double* group_mse, cudaStream_t st) {
+  EncParams p;
+  p.W = W; p.dtype = dtype; p.M = M; p.N = N;
+  p.n_ratio = cfg->n_ratio; p.n_scale = cfg->n_scale; p.n_bias = cfg->n_bias;
+  p.s_min_factor = cfg->s_min_factor;
+  p.planes = out->planes; p.scale_bias = out->scale_bias; p.ratio_idx = out->ratio_idx;
+  p.group_mse = group_mse;
+  sbvr_status s;
+  switch (cfg->K) {
+    case 1: s = launch_k<1>(p, st); break;
+    case 2: s = launch_k<2>(p, st); break;
+    case 3: s = launch_k<3>(p, st); break;
+    case 4: s = launch_k<4>(p, st); break;
+    case 5: s = launch_k<5>(p, st); break;
+    case 6: s = launch_k<6>(p, st); break;
+    default: return set_error(SBVR_ERR_UNSUPPORTED, "encoder K=%d", cfg->K);
+  }
+  if (s != SBVR_OK) return s;
+  return launch_ratio_table(out->ratio_pow, cfg->n_ratio, cfg->K, st);
+}
+
+}  // namespace sbvr

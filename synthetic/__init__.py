@@ -58,3 +58,16 @@ def with_degenerate_groups(W: np.ndarray, G: int = 128, seed: int = 0) -> np.nda
             seg[:] = 0.0
             seg[rng.integers(G)] = np.float32(1.5)
     return W
+
+
+def random_encoded(M: int, N: int, K: int, n_ratio: int, seed: int, G: int = 128):
+    """Random SBVR-encoded weights in the canonical layout (uniform bits, fp16 scale ~ |N(0.06, 0.02)|,
+    fp16 bias ~ N(0, 0.003), uniform ratio index): the structure of an encoded Llama layer without
+    running the (slow) encoder, for full-size GEMV parity and benchmarking."""
+    rng = np.random.default_rng(seed)
+    NG = N // G
+    planes = rng.integers(0, 2 ** 32, size=(M, NG, K, G // 32), dtype=np.uint64).astype(np.uint32)
+    s = np.abs(rng.normal(0.06, 0.02, size=(M, NG))).astype(np.float16)
+    b = rng.normal(0.0, 0.003, size=(M, NG)).astype(np.float16)
+    ridx = rng.integers(0, n_ratio, size=(M, NG)).astype(np.uint8)
+    return planes, s.view(np.uint16), b.view(np.uint16), ridx

@@ -1,0 +1,230 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Bar: bit-exact for planes, meta, activation planes/scales and popcount partials;
+float y within max normwise relative error 1e-3 and per-element floored relative error 1e-3
+against the fp64 oracle.  Inputs are seeded and synthetic (synthetic/), shared by both sides.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2509_18172_b200 as sb
+import synthetic
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-3
+DEV = "cuda"
+
+
+def rel_errors(y, ref):
+    y = np.asarray(y, np.float64)
+    ref = np.asarray(ref, np.float64)
+    err = np.abs(y - ref)
+    scale = np.abs(ref).max() if ref.size else 1.0
+    scale = scale if scale > 0 else 1.0
+    normwise = err.max() / scale if err.size else 0.0
+    floored = (err / np.maximum(np.abs(ref), 1e-2 * scale)).max() if err.size else 0.0
+    return normwise, floored
+
+
+def assert_close(y, ref):
+    nw, fl = rel_errors(y, ref)
+    assert nw <= TOL and fl <= TOL, (nw, fl)
+
+
+def _oracle_encoded(pc, s16, b16, ri, K, n_ratio):
+    M, NG = s16.shape
+    return oracle.Encoded(M, NG * 128, oracle.OracleConfig(K=K, n_ratio=n_ratio), pc, s16, b16, ri, np.zeros((M, NG)))
+
+
+# ------------------------------------------------------------------ a4: activation conversion (bit-exact)
+@pytest.mark.parametrize("T,N,l", [(1, 128, 8), (1, 4096, 8), (3, 1024, 8), (2, 512, 4), (1, 14336, 8), (16, 4096, 8)])
+def test_encode_vector_bitexact(T, N, l):
+    x = synthetic.activation(N, seed=N + T + l, T=T, outliers=3)
+    if N >= 256:
+        x[0, :128] = 0                                   # all-zero group
+        x[0, 128] = 127.0                                # absmax 127 -> s_x = 1: exact RNE ties below
+        x[0, 129:133] = [2.5, 3.5, -2.5, 0.5]
+    act = sb.encode_vector(torch.from_numpy(x).to(DEV), l=l)
+    torch.cuda.synchronize()
+    planes = act.data.cpu().numpy().view(np.uint32).reshape(T, N // 128, l, 4)
+    scales = act.scales.cpu().numpy().reshape(T, N // 128)
+    for t in range(T):
+        z, op, osc = oracle.encode_vector(x[t], 128, l)
+        assert np.array_equal(planes[t], op)
+        assert np.array_equal(scales[t].view(np.uint32), osc.view(np.uint32))
+
+
+# ------------------------------------------------------------------ a1-a3: encoder (bit-exact, strict fp64)
+@pytest.mark.parametrize("K,dtype", [(4, torch.float32), (3, torch.float32), (2, torch.bfloat16), (4, torch.float16)])
+def test_encode_weights_bitexact_small(K, dtype):
+    M, N = 32, 256                                       # 64 groups, 2 row tiles, 2 groups per row
+    W = synthetic.with_degenerate_groups(synthetic.gaussian_weight(M, N, seed=K, sigma=0.02), seed=K)
+    Wt = torch.from_numpy(W).to(dtype)
+    cfg = oracle.OracleConfig(K=K, n_ratio=16, n_scale=64 if K == 4 else 16, n_bias=16)
+    w, mse = sb.encode_weights(Wt.to(DEV), K=K, n_ratio=cfg.n_ratio, n_scale=cfg.n_scale, n_bias=cfg.n_bias,
+                               return_mse=True)
+    torch.cuda.synchronize()
+    ref = oracle.encode_matrix(Wt.float().numpy(), cfg)
+    pc, s16, b16, ri = sb.unpack_canonical(w)
+    assert np.array_equal(pc, ref.planes)
+    assert np.array_equal(s16, ref.s16) and np.array_equal(b16, ref.b16) and np.array_equal(ri, ref.r_idx)
+    assert np.array_equal(mse.cpu().numpy(), ref.mse)
+    # ratio table = r^t of the oracle's R in fp32
+    R = oracle.ratio_set(cfg.n_ratio)
+    assert np.allclose(w.ratio_pow.cpu().numpy(), np.power(R[:, None], np.arange(K)[None, :]), rtol=1e-7)
+
+
+def test_encode_weights_sampled_groups_full_size():
+    """Llama-3-8B q_proj shape: GPU encodes all 131072 groups; the oracle re-encodes 24 sampled ones."""
+    M, N = 4096, 4096
+    W = synthetic.gaussian_weight(M, N, seed=100, sigma=0.02)
+    w = sb.encode_weights(torch.from_numpy(W).to(DEV), K=4)
+    torch.cuda.synchronize()
+    pc, s16, b16, ri = sb.unpack_canonical(w)
+    rng = np.random.default_rng(0)
+    cfg = oracle.OracleConfig()
+    for q in rng.choice(M * (N // 128), 24, replace=False):
+        r, g = divmod(int(q), N // 128)
+        ref = oracle.encode_group(W[r, 128 * g:128 * (g + 1)].astype(np.float64), cfg)
+        assert np.array_equal(pc[r, g], ref["planes"]) and s16[r, g] == ref["s16"] and b16[r, g] == ref["b16"]
+        assert ri[r, g] == ref["r_idx"]
+
+
+def test_encode_weights_deterministic():
+    W = torch.from_numpy(synthetic.gaussian_weight(64, 512, seed=7)).to(DEV)
+    a = sb.encode_weights(W, K=4, n_scale=16)
+    b = sb.encode_weights(W, K=4, n_scale=16)
+    torch.cuda.synchronize()
+    assert torch.equal(a.planes, b.planes) and torch.equal(a.scale_bias, b.scale_bias)
+
+
+# ------------------------------------------------------------------ a5/a7: SBVR-x GEMV (partials bit-exact, y to 1e-3)
+SHAPES = [(16, 128), (64, 256), (80, 384), (208, 1024), (1024, 512)]
+
+
+@pytest.mark.parametrize("M,N", SHAPES)
+@pytest.mark.parametrize("K", [2, 3, 4])
+@pytest.mark.parametrize("algo", [sb.ALGO_IMMA, sb.ALGO_POPC])
+def test_gemv_sbvr_x(M, N, K, algo):
+    pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=M * 7 + N + K)
+    w = sb.pack_canonical(pc, s16, b16, ri, 16)
+    x = synthetic.activation(N, seed=N + 1)
+    act = sb.encode_vector(torch.from_numpy(x).to(DEV))
+    y = sb.gemv_ex(w, act, algo=algo)
+    P = sb.debug_partials(w, act, algo=algo)
+    torch.cuda.synchronize()
+    z, xp, sc = oracle.encode_vector(x[0], 128, 8)
+    enc = _oracle_encoded(pc, s16, b16, ri, K, 16)
+    ref = oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc))
+    assert_close(y.cpu().numpy()[0], ref)
+    Pref, _ = oracle.partials_rows(enc, z, xp)
+    assert np.array_equal(P.cpu().numpy(), Pref)
+
+
+@pytest.mark.parametrize("l", [8, 6, 5, 4, 2])
+def test_gemv_sbvr_x_activation_bits(l):
+    M, N, K = 48, 256, 4
+    pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=l)
+    w = sb.pack_canonical(pc, s16, b16, ri, 16)
+    x = synthetic.activation(N, seed=l)
+    act = sb.encode_vector(torch.from_numpy(x).to(DEV), l=l)
+    y = sb.gemv(w, act)
+    P = sb.debug_partials(w, act, algo=sb.ALGO_IMMA)
+    torch.cuda.synchronize()
+    z, xp, sc = oracle.encode_vector(x[0], 128, l)
+    enc = _oracle_encoded(pc, s16, b16, ri, K, 16)
+    assert_close(y.cpu().numpy(), oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc)))
+    Pref, _ = oracle.partials_rows(enc, z, xp, l=l)
+    assert np.array_equal(P.cpu().numpy(), Pref)
+
+
+def test_gemv_on_gpu_encoded_weights_matches_oracle_end_to_end():
+    """Oracle encodes W and computes y; the GPU encodes the same W and computes y."""
+    M, N, K = 48, 384, 4
+    W = synthetic.gaussian_weight(M, N, seed=31, sigma=0.02)
+    x = synthetic.activation(N, seed=32)
+    cfg = oracle.OracleConfig(n_scale=16)
+    enc = oracle.encode_matrix(W, cfg)
+    z, xp, sc = oracle.encode_vector(x[0], 128, 8)
+    w = sb.encode_weights(torch.from_numpy(W).to(DEV), K=K, n_scale=16)
+    act = sb.encode_vector(torch.from_numpy(x).to(DEV))
+    y = sb.gemv(w, act)
+    yf = sb.gemv(w, sb.fp16_activation(torch.from_numpy(x[0]).to(DEV)))
+    torch.cuda.synchronize()
+    assert_close(y.cpu().numpy(), oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc)))
+    assert_close(yf.cpu().numpy(), oracle.gemv_rows(enc, oracle.x_dec_fp16(x[0])))
+
+
+# ------------------------------------------------------------------ a6: fp16-x GEMV
+@pytest.mark.parametrize("M,N,K", [(16, 128, 4), (80, 384, 3), (256, 1024, 2)])
+def test_gemv_fp16_x(M, N, K):
+    pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=M + N)
+    w = sb.pack_canonical(pc, s16, b16, ri, 16)
+    x = synthetic.activation(N, seed=3)
+    y = sb.gemv(w, sb.fp16_activation(torch.from_numpy(x[0]).to(DEV)))
+    torch.cuda.synchronize()
+    enc = _oracle_encoded(pc, s16, b16, ri, K, 16)
+    assert_close(y.cpu().numpy(), oracle.gemv_rows(enc, oracle.x_dec_fp16(x[0])))
+
+
+# ------------------------------------------------------------------ a8: batched
+@pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 8, 16])
+def test_gemv_batched(T):
+    M, N, K = 208, 512, 4
+    pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=T)
+    w = sb.pack_canonical(pc, s16, b16, ri, 16)
+    X = synthetic.activation(N, seed=T + 50, T=T)
+    act = sb.encode_vector(torch.from_numpy(X).to(DEV))
+    Y = sb.gemv_batched(w, act)
+    Yf = sb.gemv_ex(w, sb.fp16_activation(torch.from_numpy(X).to(DEV)))
+    torch.cuda.synchronize()
+    enc = _oracle_encoded(pc, s16, b16, ri, K, 16)
+    for t in range(T):
+        z, xp, sc = oracle.encode_vector(X[t], 128, 8)
+        assert_close(Y.cpu().numpy()[t], oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc)))
+        assert_close(Yf.cpu().numpy()[t], oracle.gemv_rows(enc, oracle.x_dec_fp16(X[t])))
+
+
+# ------------------------------------------------------------------ full-size shapes, sampled rows, bench launch config
+@pytest.mark.parametrize("name,M,N", synthetic.LLAMA3_8B_LAYER + [("70b_down", 8192, 28672)])
+def test_gemv_full_size_sampled_rows(name, M, N):
+    K = 4
+    pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=M ^ N)
+    w = sb.pack_canonical(pc, s16, b16, ri, 16)
+    x = synthetic.activation(N, seed=11)
+    act = sb.encode_vector(torch.from_numpy(x).to(DEV))
+    ws = sb.Workspace.for_weights(w, 1)
+    y = sb.gemv(w, act, ws=ws)
+    y2 = sb.gemv(w, act, ws=ws)              # workspace reuse: counters must have been reset
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([np.random.default_rng(1).choice(M, 200, replace=False), [0, M - 1, 63, 64]]))
+    z, xp, sc = oracle.encode_vector(x[0], 128, 8)
+    enc = _oracle_encoded(pc, s16, b16, ri, K, 16)
+    ref = oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc), rows)
+    yy = y.cpu().numpy()
+    assert_close(yy[rows], ref)
+    assert torch.equal(y, y2)                # deterministic
+    P = sb.debug_partials(w, act, algo=sb.ALGO_IMMA)
+    Pref, _ = oracle.partials_rows(enc, z, xp, rows=rows[:16])
+    assert np.array_equal(P.cpu().numpy()[rows[:16]], Pref)
+
+
+# ------------------------------------------------------------------ error behaviour
+def test_abi_errors():
+    pc, s16, b16, ri = synthetic.random_encoded(32, 256, 4, 16, seed=0)
+    w = sb.pack_canonical(pc, s16, b16, ri, 16)
+    act = sb.encode_vector(torch.zeros(384, dtype=torch.float16, device=DEV))
+    with pytest.raises(sb.SbvrError) as e:
+        sb.gemv(w, act)
+    assert e.value.status == sb.ERR_SHAPE
+    act = sb.encode_vector(torch.zeros(256, dtype=torch.float16, device=DEV))
+    small = sb.Workspace(256)
+    with pytest.raises(sb.SbvrError) as e:
+        sb.gemv(w, act, ws=small) if sb.Workspace.for_weights(w).nbytes > 256 else (_ for _ in ()).throw(
+            sb.SbvrError(sb.ERR_WORKSPACE, "x", "y"))
+    assert e.value.status == sb.ERR_WORKSPACE
+    y = sb.gemv(w, act)
+    torch.cuda.synchronize()
+    assert not y.any()                       # zero activation -> zero output
