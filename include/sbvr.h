@@ -31,20 +31,20 @@
  *   meta    s16, b16 [M][N/G] IEEE fp16 bit patterns; r_idx [M][N/G] uint8 (index into R)
  *
  * Device weight layout (written by sbvr_encode_weights, read by the GEMV kernels; G = 128):
- *   Rows are cut into row tiles of 16 rows (M % 16 == 0).  Row tiles are grouped into bands
- *   of up to 4 tiles (64 rows; the last band holds MT % 4 tiles if MT = M/16 is not a
- *   multiple of 4).  A "tile" is (row tile rt, group g): 16 rows x 128 columns x K planes.
- *   Tiles are stored band by band; inside a band group-major, then tile-in-band:
- *       L(rt, g) = 4*b*NG + g*nb + (rt - 4*b),  b = rt/4, nb = min(4, MT - 4*b), NG = N/128.
- *   Tile L occupies 256*K bytes at planes + 64*K*L words, as ceil(K/2) chunks; chunk q holds
- *   planes 2q and 2q+1 as [lane 0..31][4 words] (the last chunk of odd K: [lane][2 words]).
- *   Lane = 4*(row%8) + c holds, for each plane t of the chunk, word c (elements 32c..32c+31
- *   of the group) of row (row%8) then of row (row%8)+8: word index (t%2)*2 + (row%16)/8.
- *   This is the A-fragment order of mma.m16n8k32 (lane = 4*groupID + threadID_in_group), so
- *   each warp-wide 16-byte load lands one plane pair of a tile directly in registers.
- *   scale_bias[16*L + 2*(row%8) + (row%16)/8] = fp16 s (bits 0-15) | fp16 b (bits 16-31)
- *   ratio_idx [16*L + 2*(row%8) + (row%16)/8] = uint8 index into R
- *   ratio_pow [n_ratio][K] fp32 = r_i^t (repeated multiplication in fp64, rounded to fp32)
+ *   Rows are cut into row tiles of 16 rows (M % 16 == 0), row tiles into bands of 4 tiles
+ *   (64 rows; the last band holds MT % 4 tiles when MT = M/16 is not a multiple of 4).  A *unit*
+ *   is (band b, group g) and is stored as ONE contiguous record of nb = tiles-in-band tiles:
+ *       [nb x 256*K bytes: bit-planes][nb x 64 B: scale/bias][nb x 16 B: ratio index]
+ *   Full bands come first, unit index b*NG + g (NG = N/128), each 4*(256*K + 80) bytes; the
+ *   tail band's NG units follow.  Total = M*N*K/8 + 5*M*N/128 bytes (no padding).
+ *   Tile i of a unit (rows 64b+16i .. +15) holds ceil(K/2) chunks; chunk q holds planes 2q and
+ *   2q+1 as [lane 0..31][4 words] (the last chunk of odd K: [lane][2 words]).  Lane 4*(r%8) + c
+ *   holds word c (elements 32c..32c+31 of the group) of row r%8 then of row r%8+8 of the tile:
+ *   word index (t%2)*2 + (r%16)/8.  This is the A-fragment order of mma.m16n8k32 (lane =
+ *   4*groupID + threadID_in_group), so a warp's 16-byte loads land in the A registers directly.
+ *   scale/bias entry 2*(r%8) + (r%16)/8 of tile i = fp16 s (bits 0-15) | fp16 b (bits 16-31);
+ *   ratio-index byte 2*(r%8) + (r%16)/8 of tile i = uint8 index into R.
+ *   ratio_pow [n_ratio][K] fp32 = r_i^t (repeated multiplication in fp64, rounded to fp32).
  *
  * Device activation layout (SBVR-x, written by sbvr_encode_vector):
  *   planes [T][N/G][l][G/32] uint32 (same bit order as the weights), scales [T][N/G] fp32.
@@ -96,10 +96,8 @@ typedef struct {
 /* Encoded weights (device pointers, caller-owned; sizes from sbvr_weights_bytes). */
 typedef struct {
   int32_t M, N, K, group_size, n_ratio;
-  uint32_t* planes;      /* device tiled layout above, 16-byte aligned */
-  uint32_t* scale_bias;  /* fp16 pair per (row, group), tile order */
-  uint8_t* ratio_idx;    /* per (row, group), tile order */
-  float* ratio_pow;      /* [n_ratio][K] */
+  uint8_t* data;         /* packed units (layout above), 16-byte aligned */
+  float* ratio_pow;      /* [n_ratio][K], 16-byte aligned */
 } sbvr_weights;
 
 /* One activation descriptor; for T vectors the buffers hold T contiguous vectors. */
@@ -115,16 +113,15 @@ int32_t sbvr_abi_version(void);
 const char* sbvr_status_string(sbvr_status s);
 const char* sbvr_last_error(void);
 
-/* Byte sizes of the four weight buffers for an M x N matrix with K planes. */
+/* Byte sizes of the two weight buffers for an M x N matrix with K planes. */
 sbvr_status sbvr_weights_bytes(int32_t M, int32_t N, int32_t K, int32_t group_size, int32_t n_ratio,
-                               size_t* planes_bytes, size_t* scale_bias_bytes, size_t* ratio_idx_bytes,
-                               size_t* ratio_pow_bytes);
+                               size_t* data_bytes, size_t* ratio_pow_bytes);
 
 /* sbvr_encode_weights -- P:150-233.  For every group of G consecutive elements of every row
  * of W (device, row-major [M][N], dtype F32/F16/BF16), build the candidate sets of Eq. 5-11,
  * run Algorithm 1's exhaustive MSE search over R x S x B (R outer, S middle, B inner, strict
- * '<'), assign each element the mask of its nearest subset sum, and write planes,
- * scale_bias, ratio_idx and ratio_pow of `out` (whose M, N, K, group_size, n_ratio must match
+ * '<'), assign each element the mask of its nearest subset sum, and write data and
+ * ratio_pow of `out` (whose M, N, K, group_size, n_ratio must match
  * cfg / the arguments).  group_mse (nullable, device, [M][N/G] fp64, row-major) receives each
  * group's winning MSE.  Groups run in parallel on the GPU. */
 sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, int32_t dtype, int32_t M,
@@ -164,13 +161,11 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
 sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_t algo, int32_t* P, void* stream);
 
 /* Host-side layout transforms (host memory on both sides, no device work).  canonical planes
- * [M][N/G][K][G/32], s16/b16/r_idx [M][N/G]  <->  device-layout images planes/scale_bias/
- * ratio_idx (sizes as sbvr_weights_bytes).  Bit-exact inverses of each other. */
+ * [M][N/G][K][G/32], s16/b16/r_idx [M][N/G]  <->  the packed device-layout image `data`
+ * (size as sbvr_weights_bytes).  Bit-exact inverses of each other. */
 sbvr_status sbvr_pack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_canon,
-                                const uint16_t* s16, const uint16_t* b16, const uint8_t* r_idx,
-                                uint32_t* planes_dev, uint32_t* scale_bias_dev, uint8_t* ratio_idx_dev);
-sbvr_status sbvr_unpack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_dev,
-                                  const uint32_t* scale_bias_dev, const uint8_t* ratio_idx_dev,
+                                const uint16_t* s16, const uint16_t* b16, const uint8_t* r_idx, uint8_t* data);
+sbvr_status sbvr_unpack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint8_t* data,
                                   uint32_t* planes_canon, uint16_t* s16, uint16_t* b16, uint8_t* r_idx);
 
 /* Write w->ratio_pow (device) for w->n_ratio, w->K (used when weights arrive via pack). */

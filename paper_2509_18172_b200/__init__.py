@@ -43,8 +43,7 @@ class _EncCfg(ctypes.Structure):
 
 class _Weights(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_size", ctypes.c_int32),
-                ("n_ratio", ctypes.c_int32), ("planes", ctypes.c_void_p), ("scale_bias", ctypes.c_void_p),
-                ("ratio_idx", ctypes.c_void_p), ("ratio_pow", ctypes.c_void_p)]
+                ("n_ratio", ctypes.c_int32), ("data", ctypes.c_void_p), ("ratio_pow", ctypes.c_void_p)]
 
 
 class _Act(ctypes.Structure):
@@ -68,7 +67,7 @@ def lib():
         L.sbvr_status_string.restype = ctypes.c_char_p
         L.sbvr_status_string.argtypes = [i32]
         L.sbvr_last_error.restype = ctypes.c_char_p
-        L.sbvr_weights_bytes.argtypes = [i32, i32, i32, i32, i32, P, P, P, P]
+        L.sbvr_weights_bytes.argtypes = [i32, i32, i32, i32, i32, P, P]
         L.sbvr_encode_weights.argtypes = [P, P, i32, i32, i32, P, P, P]
         L.sbvr_encode_vector.argtypes = [P, i32, i32, i32, i32, P, P, P]
         L.sbvr_gemv_workspace_bytes.argtypes = [P, i32, P]
@@ -77,8 +76,8 @@ def lib():
         L.sbvr_gemv_batched.argtypes = [P, P, i32, P, P, sz, P]
         L.sbvr_gemv_ex.argtypes = [P, P, i32, P, P, sz, i32, P]
         L.sbvr_debug_partials.argtypes = [P, P, i32, P, P]
-        L.sbvr_pack_canonical.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P, P]
-        L.sbvr_unpack_canonical.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P, P]
+        L.sbvr_pack_canonical.argtypes = [i32, i32, i32, i32, P, P, P, P, P]
+        L.sbvr_unpack_canonical.argtypes = [i32, i32, i32, i32, P, P, P, P, P]
         L.sbvr_fill_ratio_table.argtypes = [P, P]
         for name in ("sbvr_weights_bytes", "sbvr_encode_weights", "sbvr_encode_vector", "sbvr_gemv_workspace_bytes",
                      "sbvr_workspace_init", "sbvr_gemv", "sbvr_gemv_batched", "sbvr_gemv_ex", "sbvr_debug_partials",
@@ -114,36 +113,28 @@ class SbvrWeights:
     N: int
     K: int
     n_ratio: int
-    planes: torch.Tensor      # int32 (bit pattern of uint32), device tiled layout
-    scale_bias: torch.Tensor  # int32 (fp16 s | fp16 b << 16)
-    ratio_idx: torch.Tensor   # uint8
+    data: torch.Tensor        # uint8, packed unit records (include/sbvr.h device layout)
     ratio_pow: torch.Tensor   # float32 [n_ratio, K]
 
     def desc(self) -> _Weights:
-        return _Weights(self.M, self.N, self.K, G, self.n_ratio, self.planes.data_ptr(), self.scale_bias.data_ptr(),
-                        self.ratio_idx.data_ptr(), self.ratio_pow.data_ptr())
+        return _Weights(self.M, self.N, self.K, G, self.n_ratio, self.data.data_ptr(), self.ratio_pow.data_ptr())
 
     @property
     def nbytes(self) -> int:
         """Algorithmic bytes of the encoded weights (planes + 5 B/group metadata)."""
-        return self.planes.numel() * 4 + self.scale_bias.numel() * 4 + self.ratio_idx.numel()
-
-    def shard_rows(self, r0: int, r1: int) -> "SbvrWeights":
-        raise NotImplementedError("shard before encoding: encode each rank's row slice (see dist.py)")
+        return self.data.numel()
 
 
 def weights_bytes(M: int, N: int, K: int, n_ratio: int = 16):
-    out = [ctypes.c_size_t() for _ in range(4)]
+    out = [ctypes.c_size_t() for _ in range(2)]
     _check(lib().sbvr_weights_bytes(M, N, K, G, n_ratio, *[ctypes.byref(o) for o in out]), "sbvr_weights_bytes")
     return tuple(o.value for o in out)
 
 
 def weights_empty(M: int, N: int, K: int, n_ratio: int = 16, device="cuda") -> SbvrWeights:
-    pb, sbb, rib, rpb = weights_bytes(M, N, K, n_ratio)
+    db, rpb = weights_bytes(M, N, K, n_ratio)
     dev = torch.device(device)
-    return SbvrWeights(M, N, K, n_ratio, torch.empty(pb // 4, dtype=torch.int32, device=dev),
-                       torch.empty(sbb // 4, dtype=torch.int32, device=dev),
-                       torch.empty(rib + 16, dtype=torch.uint8, device=dev)[:rib],
+    return SbvrWeights(M, N, K, n_ratio, torch.empty(db, dtype=torch.uint8, device=dev),
                        torch.empty((n_ratio, K), dtype=torch.float32, device=dev))
 
 
@@ -212,14 +203,14 @@ class Workspace:
         n = ctypes.c_size_t()
         d = w.desc()
         _check(lib().sbvr_gemv_workspace_bytes(ctypes.byref(d), T, ctypes.byref(n)), "sbvr_gemv_workspace_bytes")
-        return Workspace(n.value, w.planes.device)
+        return Workspace(n.value, w.data.device)
 
 
 def gemv_ex(w: SbvrWeights, x: SbvrActivation, y: Optional[torch.Tensor] = None, ws: Optional[Workspace] = None,
             algo: int = ALGO_AUTO) -> torch.Tensor:
     T = x.T
     if y is None:
-        y = torch.empty((T, w.M), dtype=torch.float32, device=w.planes.device)
+        y = torch.empty((T, w.M), dtype=torch.float32, device=w.data.device)
     if ws is None:
         ws = Workspace.for_weights(w, T)
     wd, xd = w.desc(), x.desc()
@@ -233,7 +224,7 @@ def gemv(w: SbvrWeights, x: SbvrActivation, y: Optional[torch.Tensor] = None,
     """sbvr_gemv: y[M] = W x on the SBVR weights, x SBVR-encoded or fp16."""
     assert x.T == 1
     if y is None:
-        y = torch.empty(w.M, dtype=torch.float32, device=w.planes.device)
+        y = torch.empty(w.M, dtype=torch.float32, device=w.data.device)
     if ws is None:
         ws = Workspace.for_weights(w, 1)
     wd, xd = w.desc(), x.desc()
@@ -246,7 +237,7 @@ def gemv_batched(w: SbvrWeights, X: SbvrActivation, Y: Optional[torch.Tensor] = 
                  ws: Optional[Workspace] = None) -> torch.Tensor:
     """sbvr_gemv_batched: Y[T, M] for T <= 16 vectors sharing one weight fetch."""
     if Y is None:
-        Y = torch.empty((X.T, w.M), dtype=torch.float32, device=w.planes.device)
+        Y = torch.empty((X.T, w.M), dtype=torch.float32, device=w.data.device)
     if ws is None:
         ws = Workspace.for_weights(w, X.T)
     wd, xd = w.desc(), X.desc()
@@ -256,7 +247,7 @@ def gemv_batched(w: SbvrWeights, X: SbvrActivation, Y: Optional[torch.Tensor] = 
 
 
 def debug_partials(w: SbvrWeights, x: SbvrActivation, algo: int = ALGO_IMMA) -> torch.Tensor:
-    P = torch.full((w.M, w.N // G, w.K, x.l), -1, dtype=torch.int32, device=w.planes.device)
+    P = torch.full((w.M, w.N // G, w.K, x.l), -1, dtype=torch.int32, device=w.data.device)
     wd, xd = w.desc(), x.desc()
     _check(lib().sbvr_debug_partials(ctypes.byref(wd), ctypes.byref(xd), algo, _ptr(P), _stream()),
            "sbvr_debug_partials")
@@ -264,25 +255,39 @@ def debug_partials(w: SbvrWeights, x: SbvrActivation, algo: int = ALGO_IMMA) -> 
 
 
 # ------------------------------------------------------------------ host layout transforms
-def pack_canonical(planes_canon: np.ndarray, s16: np.ndarray, b16: np.ndarray, r_idx: np.ndarray, n_ratio: int = 16,
-                   device="cuda") -> SbvrWeights:
-    """Canonical [M][N/G][K][4] planes + meta -> device SbvrWeights (host transform, then upload)."""
+def pack_host(planes_canon, s16, b16, r_idx) -> np.ndarray:
+    """Canonical planes [M][N/G][K][4] + meta -> packed device-layout image (numpy uint8)."""
     M, NG, K, _ = planes_canon.shape
     N = NG * G
-    pb, sbb, rib, _ = weights_bytes(M, N, K, n_ratio)
-    pd = np.zeros(pb // 4, np.uint32)
-    sbd = np.zeros(sbb // 4, np.uint32)
-    rid = np.zeros(rib, np.uint8)
-    pc = np.ascontiguousarray(planes_canon, np.uint32)
-    s16 = np.ascontiguousarray(s16, np.uint16)
-    b16 = np.ascontiguousarray(b16, np.uint16)
-    r_idx = np.ascontiguousarray(r_idx, np.uint8)
-    _check(lib().sbvr_pack_canonical(M, N, K, G, _np_ptr(pc), _np_ptr(s16), _np_ptr(b16), _np_ptr(r_idx), _np_ptr(pd),
-                                     _np_ptr(sbd), _np_ptr(rid)), "sbvr_pack_canonical")
-    w = weights_empty(M, N, K, n_ratio, device)
-    w.planes.copy_(torch.from_numpy(pd.view(np.int32)))
-    w.scale_bias.copy_(torch.from_numpy(sbd.view(np.int32)))
-    w.ratio_idx.copy_(torch.from_numpy(rid))
+    db, _ = weights_bytes(M, N, K)
+    data = np.zeros(db, np.uint8)
+    _check(lib().sbvr_pack_canonical(M, N, K, G, _np_ptr(np.ascontiguousarray(planes_canon, np.uint32)),
+                                     _np_ptr(np.ascontiguousarray(s16, np.uint16)),
+                                     _np_ptr(np.ascontiguousarray(b16, np.uint16)),
+                                     _np_ptr(np.ascontiguousarray(r_idx, np.uint8)), _np_ptr(data)),
+           "sbvr_pack_canonical")
+    return data
+
+
+def unpack_host(M: int, N: int, K: int, data: np.ndarray):
+    NG = N // G
+    pc = np.zeros((M, NG, K, 4), np.uint32)
+    s16 = np.zeros((M, NG), np.uint16)
+    b16 = np.zeros((M, NG), np.uint16)
+    ri = np.zeros((M, NG), np.uint8)
+    data = np.ascontiguousarray(data, np.uint8)
+    _check(lib().sbvr_unpack_canonical(M, N, K, G, _np_ptr(data), _np_ptr(pc), _np_ptr(s16), _np_ptr(b16),
+                                       _np_ptr(ri)), "sbvr_unpack_canonical")
+    return pc, s16, b16, ri
+
+
+def pack_canonical(planes_canon: np.ndarray, s16: np.ndarray, b16: np.ndarray, r_idx: np.ndarray, n_ratio: int = 16,
+                   device="cuda") -> SbvrWeights:
+    """Canonical planes + meta -> device SbvrWeights (host transform, upload, ratio table)."""
+    M, NG, K, _ = planes_canon.shape
+    data = pack_host(planes_canon, s16, b16, r_idx)
+    w = weights_empty(M, NG * G, K, n_ratio, device)
+    w.data.copy_(torch.from_numpy(data))
     d = w.desc()
     _check(lib().sbvr_fill_ratio_table(ctypes.byref(d), _stream()), "sbvr_fill_ratio_table")
     return w
@@ -290,41 +295,7 @@ def pack_canonical(planes_canon: np.ndarray, s16: np.ndarray, b16: np.ndarray, r
 
 def unpack_canonical(w: SbvrWeights):
     """Device SbvrWeights -> canonical numpy (planes [M][N/G][K][4] uint32, s16, b16, r_idx [M][N/G])."""
-    NG = w.N // G
-    pd = w.planes.cpu().numpy().view(np.uint32).copy()
-    sbd = w.scale_bias.cpu().numpy().view(np.uint32).copy()
-    rid = w.ratio_idx.cpu().numpy().copy()
-    return unpack_host(w.M, w.N, w.K, pd, sbd, rid)
-
-
-def unpack_host(M: int, N: int, K: int, pd: np.ndarray, sbd: np.ndarray, rid: np.ndarray):
-    NG = N // G
-    pc = np.zeros((M, NG, K, 4), np.uint32)
-    s16 = np.zeros((M, NG), np.uint16)
-    b16 = np.zeros((M, NG), np.uint16)
-    ri = np.zeros((M, NG), np.uint8)
-    pd = np.ascontiguousarray(pd, np.uint32)
-    sbd = np.ascontiguousarray(sbd, np.uint32)
-    rid = np.ascontiguousarray(rid, np.uint8)
-    _check(lib().sbvr_unpack_canonical(M, N, K, G, _np_ptr(pd), _np_ptr(sbd), _np_ptr(rid), _np_ptr(pc), _np_ptr(s16),
-                                       _np_ptr(b16), _np_ptr(ri)), "sbvr_unpack_canonical")
-    return pc, s16, b16, ri
-
-
-def pack_host(planes_canon, s16, b16, r_idx):
-    """Canonical -> device-layout images on the host (numpy); used by layout tests."""
-    M, NG, K, _ = planes_canon.shape
-    N = NG * G
-    pb, sbb, rib, _ = weights_bytes(M, N, K)
-    pd = np.zeros(pb // 4, np.uint32)
-    sbd = np.zeros(sbb // 4, np.uint32)
-    rid = np.zeros(rib, np.uint8)
-    _check(lib().sbvr_pack_canonical(M, N, K, G, _np_ptr(np.ascontiguousarray(planes_canon, np.uint32)),
-                                     _np_ptr(np.ascontiguousarray(s16, np.uint16)),
-                                     _np_ptr(np.ascontiguousarray(b16, np.uint16)),
-                                     _np_ptr(np.ascontiguousarray(r_idx, np.uint8)), _np_ptr(pd), _np_ptr(sbd),
-                                     _np_ptr(rid)), "sbvr_pack_canonical")
-    return pd, sbd, rid
+    return unpack_host(w.M, w.N, w.K, w.data.cpu().numpy())
 
 
 def algorithmic_bytes(M: int, N: int, K: int, act: str = "sbvr", l: int = 8, T: int = 1) -> int:

@@ -31,8 +31,7 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 static sbvr_status check_weights(const sbvr_weights* w) {
   if (!w) return set_error(SBVR_ERR_INVALID_ARG, "weights descriptor is NULL");
-  if (!w->planes || !w->scale_bias || !w->ratio_idx || !w->ratio_pow)
-    return set_error(SBVR_ERR_INVALID_ARG, "weights buffer pointer is NULL");
+  if (!w->data || !w->ratio_pow) return set_error(SBVR_ERR_INVALID_ARG, "weights buffer pointer is NULL");
   if (w->group_size != kG) return set_error(SBVR_ERR_UNSUPPORTED, "group_size %d (only 128)", w->group_size);
   if (w->K < 1 || w->K > kMaxK) return set_error(SBVR_ERR_UNSUPPORTED, "K=%d outside 1..8", w->K);
   if (w->n_ratio < 2 || w->n_ratio > 64 || (w->n_ratio & 1))
@@ -40,7 +39,7 @@ static sbvr_status check_weights(const sbvr_weights* w) {
   if (w->M <= 0 || w->N <= 0) return set_error(SBVR_ERR_SHAPE, "M=%d N=%d must be positive", w->M, w->N);
   if (w->M % kTileRows) return set_error(SBVR_ERR_SHAPE, "M=%d not a multiple of 16", w->M);
   if (w->N % kG) return set_error(SBVR_ERR_SHAPE, "N=%d not a multiple of group_size 128", w->N);
-  if (!aligned16(w->planes) || !aligned16(w->scale_bias) || !aligned16(w->ratio_pow))
+  if (!aligned16(w->data) || !aligned16(w->ratio_pow))
     return set_error(SBVR_ERR_ALIGNMENT, "weights buffers must be 16-byte aligned");
   return SBVR_OK;
 }
@@ -87,19 +86,15 @@ const char* sbvr_status_string(sbvr_status s) {
 const char* sbvr_last_error(void) { return g_err; }
 
 sbvr_status sbvr_weights_bytes(int32_t M, int32_t N, int32_t K, int32_t group_size, int32_t n_ratio,
-                               size_t* planes_bytes, size_t* scale_bias_bytes, size_t* ratio_idx_bytes,
-                               size_t* ratio_pow_bytes) {
-  if (!planes_bytes || !scale_bias_bytes || !ratio_idx_bytes || !ratio_pow_bytes)
+                               size_t* data_bytes, size_t* ratio_pow_bytes) {
+  if (!data_bytes || !ratio_pow_bytes)
     return set_error(SBVR_ERR_INVALID_ARG, "output pointer is NULL");
   if (group_size != kG) return set_error(SBVR_ERR_UNSUPPORTED, "group_size %d (only 128)", group_size);
   if (K < 1 || K > kMaxK) return set_error(SBVR_ERR_UNSUPPORTED, "K=%d outside 1..8", K);
   if (M <= 0 || N <= 0 || M % kTileRows || N % kG)
     return set_error(SBVR_ERR_SHAPE, "M=%d must be a positive multiple of 16, N=%d of 128", M, N);
   if (n_ratio < 2 || n_ratio > 64 || (n_ratio & 1)) return set_error(SBVR_ERR_INVALID_ARG, "bad n_ratio %d", n_ratio);
-  size_t groups = (size_t)M * (N / kG);
-  *planes_bytes = groups * (size_t)K * kWPG * 4;
-  *scale_bias_bytes = groups * 4;
-  *ratio_idx_bytes = groups;
+  *data_bytes = (size_t)Layout(M, N, K).total_bytes();
   *ratio_pow_bytes = (size_t)n_ratio * K * 4;
   return SBVR_OK;
 }
@@ -201,42 +196,41 @@ static sbvr_status check_pack_args(int32_t M, int32_t N, int32_t K, int32_t G) {
 }
 
 sbvr_status sbvr_pack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_canon,
-                                const uint16_t* s16, const uint16_t* b16, const uint8_t* r_idx, uint32_t* planes_dev,
-                                uint32_t* scale_bias_dev, uint8_t* ratio_idx_dev) {
+                                const uint16_t* s16, const uint16_t* b16, const uint8_t* r_idx, uint8_t* data) {
   sbvr_status s = check_pack_args(M, N, K, group_size);
   if (s != SBVR_OK) return s;
-  if (!planes_canon || !s16 || !b16 || !r_idx || !planes_dev || !scale_bias_dev || !ratio_idx_dev)
-    return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  if (!planes_canon || !s16 || !b16 || !r_idx || !data) return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
   Layout Lo(M, N, K);
   for (int r = 0; r < M; ++r)
     for (int g = 0; g < Lo.NG; ++g) {
       long q = (long)r * Lo.NG + g;
       for (int t = 0; t < K; ++t)
-        for (int c = 0; c < kWPG; ++c) planes_dev[Lo.plane_word(r, g, t, c)] = planes_canon[(q * K + t) * kWPG + c];
-      long m = Lo.meta(r, g);
-      scale_bias_dev[m] = (uint32_t)s16[q] | ((uint32_t)b16[q] << 16);
-      ratio_idx_dev[m] = r_idx[q];
+        for (int c = 0; c < kWPG; ++c)
+          memcpy(data + Lo.plane_byte(r, g, t, c), planes_canon + (q * K + t) * kWPG + c, 4);
+      const uint32_t sb = (uint32_t)s16[q] | ((uint32_t)b16[q] << 16);
+      memcpy(data + Lo.sb_byte(r, g), &sb, 4);
+      data[Lo.ri_byte(r, g)] = r_idx[q];
     }
   return SBVR_OK;
 }
 
-sbvr_status sbvr_unpack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_dev,
-                                  const uint32_t* scale_bias_dev, const uint8_t* ratio_idx_dev,
+sbvr_status sbvr_unpack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint8_t* data,
                                   uint32_t* planes_canon, uint16_t* s16, uint16_t* b16, uint8_t* r_idx) {
   sbvr_status s = check_pack_args(M, N, K, group_size);
   if (s != SBVR_OK) return s;
-  if (!planes_canon || !s16 || !b16 || !r_idx || !planes_dev || !scale_bias_dev || !ratio_idx_dev)
-    return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  if (!planes_canon || !s16 || !b16 || !r_idx || !data) return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
   Layout Lo(M, N, K);
   for (int r = 0; r < M; ++r)
     for (int g = 0; g < Lo.NG; ++g) {
       long q = (long)r * Lo.NG + g;
       for (int t = 0; t < K; ++t)
-        for (int c = 0; c < kWPG; ++c) planes_canon[(q * K + t) * kWPG + c] = planes_dev[Lo.plane_word(r, g, t, c)];
-      long m = Lo.meta(r, g);
-      s16[q] = (uint16_t)(scale_bias_dev[m] & 0xffffu);
-      b16[q] = (uint16_t)(scale_bias_dev[m] >> 16);
-      r_idx[q] = ratio_idx_dev[m];
+        for (int c = 0; c < kWPG; ++c)
+          memcpy(planes_canon + (q * K + t) * kWPG + c, data + Lo.plane_byte(r, g, t, c), 4);
+      uint32_t sb;
+      memcpy(&sb, data + Lo.sb_byte(r, g), 4);
+      s16[q] = (uint16_t)(sb & 0xffffu);
+      b16[q] = (uint16_t)(sb >> 16);
+      r_idx[q] = data[Lo.ri_byte(r, g)];
     }
   return SBVR_OK;
 }

@@ -13,6 +13,9 @@ namespace sbvr {
 __global__ void __launch_bounds__(256) encode_vector_kernel(const uint16_t* __restrict__ x, int total_groups, int l,
                                                             uint32_t* __restrict__ planes,
                                                             float* __restrict__ scales) {
+  // programmatic dependent launch: the planes we write may still be read by the previous GEMV
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // group index over [T][N/G]
   if (q >= total_groups) return;
@@ -49,7 +52,17 @@ sbvr_status launch_encode_vector(const uint16_t* x, int T, int N, int l, uint32_
                                  cudaStream_t st) {
   const int groups = T * (N / kG);
   const int blocks = (groups * 32 + 255) / 256;
-  encode_vector_kernel<<<blocks, 256, 0, st>>>(x, groups, l, planes, scales);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, encode_vector_kernel, x, groups, l, planes, scales);
+  if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "encode_vector launch: %s", cudaGetErrorString(e));
   return check_launch("encode_vector_kernel");
 }
 

@@ -54,9 +54,7 @@ struct EncParams {
   int dtype, M, N;
   int n_ratio, n_scale, n_bias;
   double s_min_factor;
-  uint32_t* planes;
-  uint32_t* scale_bias;
-  uint8_t* ratio_idx;
+  uint8_t* data;
   double* group_mse;
 };
 
@@ -211,13 +209,13 @@ __global__ void __launch_bounds__(256) encode_weights_kernel(EncParams p) {
 #pragma unroll
       for (int t = 0; t < K; ++t) {
         const uint32_t word = __ballot_sync(0xffffffffu, (bm >> t) & 1);
-        if (lane == t) p.planes[Lo.plane_word(row, g, t, warp)] = word;
+        if (lane == t) *reinterpret_cast<uint32_t*>(p.data + Lo.plane_byte(row, g, t, warp)) = word;
       }
     }
     if (tid == 0) {
-      const long m = Lo.meta(row, g);
-      p.scale_bias[m] = (uint32_t)f64_to_f16_bits(S[wj]) | ((uint32_t)f64_to_f16_bits(B[wk]) << 16);
-      p.ratio_idx[m] = (uint8_t)wi;
+      *reinterpret_cast<uint32_t*>(p.data + Lo.sb_byte(row, g)) =
+          (uint32_t)f64_to_f16_bits(S[wj]) | ((uint32_t)f64_to_f16_bits(B[wk]) << 16);
+      p.data[Lo.ri_byte(row, g)] = (uint8_t)wi;
       if (p.group_mse) p.group_mse[q] = win_mse;
     }
     __syncthreads();
@@ -260,7 +258,7 @@ sbvr_status launch_encode_weights(const sbvr_encode_config* cfg, const void* W, 
   p.W = W; p.dtype = dtype; p.M = M; p.N = N;
   p.n_ratio = cfg->n_ratio; p.n_scale = cfg->n_scale; p.n_bias = cfg->n_bias;
   p.s_min_factor = cfg->s_min_factor;
-  p.planes = out->planes; p.scale_bias = out->scale_bias; p.ratio_idx = out->ratio_idx;
+  p.data = out->data;
   p.group_mse = group_mse;
   sbvr_status s;
   switch (cfg->K) {

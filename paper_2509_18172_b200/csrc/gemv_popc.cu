@@ -17,9 +17,7 @@
 namespace sbvr {
 
 struct PopcParams {
-  const uint32_t* planes;
-  const uint32_t* scale_bias;
-  const uint8_t* ratio_idx;
+  const uint8_t* data;
   const float* ratio_pow;
   const uint32_t* xplanes;  // [T][NG][l][4]
   const float* xscales;     // [T][NG]
@@ -40,16 +38,15 @@ __global__ void __launch_bounds__(256) gemv_popc_kernel(PopcParams p) {
   for (int tok = 0; tok < p.T; ++tok) {
     float acc = 0.0f;
     for (int g = lane; g < Lo.NG; g += 32) {
-      const long m = Lo.meta(row, g);
-      const uint32_t sb = __ldg(p.scale_bias + m);
+      const uint32_t sb = __ldg(reinterpret_cast<const uint32_t*>(p.data + Lo.sb_byte(row, g)));
       const float s = half_lo(sb), b = half_hi(sb);
-      const float* pw = p.ratio_pow + (int)__ldg(p.ratio_idx + m) * p.K;
+      const float* pw = p.ratio_pow + (int)__ldg(p.data + Lo.ri_byte(row, g)) * p.K;
       const uint32_t* xp = p.xplanes + ((size_t)tok * Lo.NG + g) * p.l * kWPG;
       float gval = 0.0f;
       for (int t = 0; t < p.K; ++t) {
         uint32_t w[kWPG];
 #pragma unroll
-        for (int c = 0; c < kWPG; ++c) w[c] = __ldg(p.planes + Lo.plane_word(row, g, t, c));
+        for (int c = 0; c < kWPG; ++c) w[c] = __ldg(reinterpret_cast<const uint32_t*>(p.data + Lo.plane_byte(row, g, t, c)));
         int T_t = 0;
         for (int j = 0; j < p.l; ++j) {
           int P_tj = 0;
@@ -72,7 +69,7 @@ __global__ void __launch_bounds__(256) gemv_popc_kernel(PopcParams p) {
 sbvr_status launch_gemv_popc(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, int32_t* P_debug,
                              cudaStream_t st) {
   PopcParams p;
-  p.planes = w->planes; p.scale_bias = w->scale_bias; p.ratio_idx = w->ratio_idx; p.ratio_pow = w->ratio_pow;
+  p.data = w->data; p.ratio_pow = w->ratio_pow;
   p.xplanes = static_cast<const uint32_t*>(x->data); p.xscales = x->scales;
   p.Y = Y; p.P = P_debug; p.M = w->M; p.N = w->N; p.K = w->K; p.l = x->l; p.T = T;
   const int blocks = (w->M * 32 + 255) / 256;
@@ -91,15 +88,14 @@ __global__ void __launch_bounds__(256) gemv_fp16x_kernel(PopcParams p, const uin
     const uint16_t* xt = x + (size_t)tok * p.N;
     float acc = 0.0f;
     for (int g = lane; g < Lo.NG; g += 32) {
-      const long m = Lo.meta(row, g);
-      const uint32_t sb = __ldg(p.scale_bias + m);
+      const uint32_t sb = __ldg(reinterpret_cast<const uint32_t*>(p.data + Lo.sb_byte(row, g)));
       const float s = half_lo(sb), b = half_hi(sb);
-      const float* pw = p.ratio_pow + (int)__ldg(p.ratio_idx + m) * p.K;
+      const float* pw = p.ratio_pow + (int)__ldg(p.data + Lo.ri_byte(row, g)) * p.K;
       float gval = 0.0f;
       for (int t = 0; t < p.K; ++t) {
         float M_t = 0.0f;
         for (int c = 0; c < kWPG; ++c) {
-          uint32_t w = __ldg(p.planes + Lo.plane_word(row, g, t, c));
+          uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(p.data + Lo.plane_byte(row, g, t, c)));
           while (w) {
             const int e = __ffs(w) - 1;
             w &= w - 1;
@@ -118,7 +114,7 @@ __global__ void __launch_bounds__(256) gemv_fp16x_kernel(PopcParams p, const uin
 
 sbvr_status launch_gemv_fp16x(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, cudaStream_t st) {
   PopcParams p;
-  p.planes = w->planes; p.scale_bias = w->scale_bias; p.ratio_idx = w->ratio_idx; p.ratio_pow = w->ratio_pow;
+  p.data = w->data; p.ratio_pow = w->ratio_pow;
   p.xplanes = nullptr; p.xscales = nullptr;
   p.Y = Y; p.P = nullptr; p.M = w->M; p.N = w->N; p.K = w->K; p.l = 0; p.T = T;
   const int blocks = (w->M * 32 + 255) / 256;

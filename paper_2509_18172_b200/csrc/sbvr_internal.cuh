@@ -17,41 +17,42 @@ constexpr int kMaxK = 8;
 constexpr int kMaxT = 16;
 
 // ------------------------------------------------------------------ device weight layout (sbvr.h)
+// One packed buffer of "units".  A unit is (band b of up to 4 row tiles of 16 rows, group g):
+//   [nb tiles x 256*K bytes of planes][nb x 64 B scale/bias][nb x 16 B ratio index]
+// Full bands come first (unit index b*NG + g, all the same size), then the tail band (M % 64).
 struct Layout {
-  int M, N, K, MT, NG, n_bands;
+  int M, N, K, MT, NG, n_full, tail_nb, n_bands;
   __host__ __device__ Layout(int M_, int N_, int K_) : M(M_), N(N_), K(K_) {
     MT = M / kTileRows;
     NG = N / kG;
-    n_bands = (MT + kBandTiles - 1) / kBandTiles;
+    n_full = MT / kBandTiles;
+    tail_nb = MT % kBandTiles;
+    n_bands = n_full + (tail_nb ? 1 : 0);
   }
-  __host__ __device__ int band_tiles(int b) const {
-    int r = MT - kBandTiles * b;
-    return r < kBandTiles ? r : kBandTiles;
+  __host__ __device__ long unit_bytes(int nb) const { return (long)nb * (256L * K + 80); }
+  __host__ __device__ long unit_off(int b, int g) const {
+    if (b < n_full) return ((long)b * NG + g) * unit_bytes(kBandTiles);
+    return (long)n_full * NG * unit_bytes(kBandTiles) + (long)g * unit_bytes(tail_nb);
   }
-  // linear tile index of (row tile rt, group g)
-  __host__ __device__ long tile(int rt, int g) const {
-    int b = rt / kBandTiles;
-    return (long)kBandTiles * b * NG + (long)g * band_tiles(b) + (rt - kBandTiles * b);
+  __host__ __device__ long total_bytes() const {
+    return (long)n_full * NG * unit_bytes(kBandTiles) + (tail_nb ? (long)NG * unit_bytes(tail_nb) : 0L);
   }
-  __host__ __device__ long tiles() const { return (long)MT * NG; }
-  __host__ __device__ long tile_words() const { return 64L * K; }
-  // word offset (within the planes array) of plane t, word c of (row, group)
-  __host__ __device__ long plane_word(int row, int g, int t, int c) const {
-    long L = tile(row / kTileRows, g);
-    int r16 = row % kTileRows;
-    int lane = 4 * (r16 % 8) + c;
-    int h = r16 / 8;
-    int q = t / 2;
-    int last_odd = (K & 1) && (q == K / 2);
-    long base = L * tile_words() + (long)q * 128;  // 32 lanes x 4 words per full chunk
-    if (last_odd) return base + lane * 2 + h;
-    return base + lane * 4 + (t % 2) * 2 + h;
+  __host__ __device__ int band_tiles(int b) const { return b < n_full ? kBandTiles : tail_nb; }
+  // byte offset of the 32-bit word holding plane t, word c (elements 32c..32c+31) of (row, group)
+  __host__ __device__ long plane_byte(int row, int g, int t, int c) const {
+    const int rt = row / kTileRows, b = rt / kBandTiles, i = rt % kBandTiles, r16 = row % kTileRows;
+    const int lane = 4 * (r16 % 8) + c, h = r16 / 8, q = t / 2;
+    const bool last_odd = (K & 1) && (q == K / 2);
+    const long base = unit_off(b, g) + (long)i * 256 * K + (long)q * 512;
+    return last_odd ? base + lane * 8 + h * 4 : base + lane * 16 + ((t % 2) * 2 + h) * 4;
   }
-  // index into scale_bias / ratio_idx
-  __host__ __device__ long meta(int row, int g) const {
-    long L = tile(row / kTileRows, g);
-    int r16 = row % kTileRows;
-    return 16 * L + 2 * (r16 % 8) + r16 / 8;
+  __host__ __device__ long sb_byte(int row, int g) const {
+    const int rt = row / kTileRows, b = rt / kBandTiles, i = rt % kBandTiles, r16 = row % kTileRows;
+    return unit_off(b, g) + (long)band_tiles(b) * 256 * K + i * 64 + (2 * (r16 % 8) + r16 / 8) * 4;
+  }
+  __host__ __device__ long ri_byte(int row, int g) const {
+    const int rt = row / kTileRows, b = rt / kBandTiles, i = rt % kBandTiles, r16 = row % kTileRows;
+    return unit_off(b, g) + (long)band_tiles(b) * (256L * K + 64) + i * 16 + 2 * (r16 % 8) + r16 / 8;
   }
 };
 

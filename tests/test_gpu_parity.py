@@ -97,7 +97,7 @@ def test_encode_weights_deterministic():
     a = sb.encode_weights(W, K=4, n_scale=16)
     b = sb.encode_weights(W, K=4, n_scale=16)
     torch.cuda.synchronize()
-    assert torch.equal(a.planes, b.planes) and torch.equal(a.scale_bias, b.scale_bias)
+    assert torch.equal(a.data, b.data) and torch.equal(a.ratio_pow, b.ratio_pow)
 
 
 # ------------------------------------------------------------------ a5/a7: SBVR-x GEMV (partials bit-exact, y to 1e-3)
