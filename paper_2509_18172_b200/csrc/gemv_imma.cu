@@ -62,6 +62,7 @@ struct ImmaParams {
   int Us;                   // units in this launch
   int Pw, qq, rr;           // CTAs and the unit partition over CTAs
   int exp_mode;             // ablation bits (env SBVR_EXP_MODE), 0 in production
+  int one;                  // = 1 (runtime value, see i2f_fma)
   unsigned long long* ts;   // phase timestamps (exp_mode & 8)
 };
 __device__ __forceinline__ unsigned long long gtime() {
@@ -112,6 +113,13 @@ __device__ __forceinline__ void mma_u8(int (&d)[4], uint32_t a0, uint32_t a1, ui
   asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};"
       : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
+}
+
+// exact int -> float for |u| < 2^22 without the ALU pipe: (u + 0x4B400000) as float - 12582912
+__device__ __forceinline__ float i2f_fma(int u, int one) {
+  int v;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(v) : "r"(u), "r"(one), "r"(0x4B400000));
+  return __int_as_float(v) - 12582912.0f;
 }
 
 __device__ __forceinline__ int imad(int a, int b, int c) {
@@ -234,6 +242,9 @@ __global__ void __launch_bounds__(kImmaWarps * 32, TT == 1 ? 2 : 1) gemv_imma_ke
     const int al1 = j1 < p.l - 1 ? (1 << j1) : (j1 == p.l - 1 ? -(1 << j1) : 0);
     const int kappa = al0 != 0 ? al1 / al0 : 0;
     const float lane_scale = (float)al0 * (1.0f / 128.0f);
+    const int one = p.one;                          // runtime 1 keeps the conversion IMADs on the FMA pipe
+    // lanes whose activation plane gq >= l contribute 0: their B words are masked at use time
+    const uint32_t xmask = gq < p.l ? 0xffffffffu : 0u;
     const uint32_t* xlane_ptr = p.xplanes + (gq < p.l ? gq * 4 + c : 0);
     const int xstride = p.l * 4;
 
@@ -251,8 +262,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, TT == 1 ? 2 : 1) gemv_imma_ke
     float sxn[TT];
 #pragma unroll
     for (int tk = 0; tk < TT; ++tk) {
-      const uint32_t xv = __ldg(xlane_ptr + ((size_t)tk * NG + g) * xstride);
-      Xn[tk] = gq < p.l ? xv : 0u;
+      Xn[tk] = __ldg(xlane_ptr + ((size_t)tk * NG + g) * xstride);
       sxn[tk] = __ldg(p.xscales + (size_t)tk * NG + g);
     }
 
@@ -263,10 +273,11 @@ __global__ void __launch_bounds__(kImmaWarps * 32, TT == 1 ? 2 : 1) gemv_imma_ke
 #pragma unroll
       for (int tk = 0; tk < TT; ++tk) {
         sx[tk] = sxn[tk];
+        const uint32_t X = Xn[tk] & xmask;
 #pragma unroll
         for (int pr = 0; pr < 4; ++pr) {
-          Bq[tk][pr][0] = bslice(Xn[tk], 2 * pr);
-          Bq[tk][pr][1] = bslice(Xn[tk], 2 * pr + 1);
+          Bq[tk][pr][0] = bslice(X, 2 * pr);
+          Bq[tk][pr][1] = bslice(X, 2 * pr + 1);
         }
       }
       // next unit of this warp (kImmaWarps further): band/group incrementally, activation prefetch
@@ -277,15 +288,13 @@ __global__ void __launch_bounds__(kImmaWarps * 32, TT == 1 ? 2 : 1) gemv_imma_ke
         const int gp = has_next ? gn : g;
 #pragma unroll
         for (int tk = 0; tk < TT; ++tk) {
-          const uint32_t xv = __ldg(xlane_ptr + ((size_t)tk * NG + gp) * xstride);
-          Xn[tk] = gq < p.l ? xv : 0u;
+          Xn[tk] = __ldg(xlane_ptr + ((size_t)tk * NG + gp) * xstride);
           sxn[tk] = __ldg(p.xscales + (size_t)tk * NG + gp);
         }
       }
 
       uint8_t* sl = ring + slot * Gm::kSlotBytes;
       mbar_wait(bars + slot, phase);
-      if (k == 0 && wib == 0) TSW(1);
 
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
@@ -340,14 +349,15 @@ __global__ void __launch_bounds__(kImmaWarps * 32, TT == 1 ? 2 : 1) gemv_imma_ke
           const float b1 = __half2float(__ushort_as_half((unsigned short)(sbp.y >> 16)));
 #pragma unroll
           for (int tk = 0; tk < TT; ++tk) {
-            // u_t = 128 (P_2c + kappa P_2c+1) exact; sum_t r^t u_t by Horner; sum_t u_t
-            float Ph0 = __int2float_rn(imad(D[tk][K - 1][1], kappa, D[tk][K - 1][0]));
-            float Ph1 = __int2float_rn(imad(D[tk][K - 1][3], kappa, D[tk][K - 1][2]));
+            // u_t = 128 (P_2c + kappa P_2c+1), exact and |u_t| < 2^22: converted on the FMA pipe as
+            // float_bits(u_t + 0x4B400000) - 1.5*2^23 (the ALU pipe is busy with the A extraction)
+            float Ph0 = i2f_fma(imad(D[tk][K - 1][1], kappa, D[tk][K - 1][0]), one);
+            float Ph1 = i2f_fma(imad(D[tk][K - 1][3], kappa, D[tk][K - 1][2]), one);
             float U0 = Ph0, U1 = Ph1;
 #pragma unroll
             for (int t = K - 2; t >= 0; --t) {
-              const float f0 = __int2float_rn(imad(D[tk][t][1], kappa, D[tk][t][0]));
-              const float f1 = __int2float_rn(imad(D[tk][t][3], kappa, D[tk][t][2]));
+              const float f0 = i2f_fma(imad(D[tk][t][1], kappa, D[tk][t][0]), one);
+              const float f1 = i2f_fma(imad(D[tk][t][3], kappa, D[tk][t][2]), one);
               Ph0 = fmaf(Ph0, r0, f0);
               Ph1 = fmaf(Ph1, r1, f1);
               U0 += f0;
@@ -554,6 +564,7 @@ sbvr_status launch_gemv_imma(const sbvr_weights* w, const sbvr_act* x, int T, fl
   p.ratio_pow = w->ratio_pow;
   p.M = w->M; p.N = w->N; p.l = x->l; p.n_ratio = w->n_ratio;
   p.P = P_debug;
+  p.one = 1;
   {
     const char* em = getenv("SBVR_EXP_MODE");
     p.exp_mode = em ? atoi(em) : 0;
