@@ -31,19 +31,19 @@
  *   meta    s16, b16 [M][N/G] IEEE fp16 bit patterns; r_idx [M][N/G] uint8 (index into R)
  *
  * Device weight layout (written by sbvr_encode_weights, read by the GEMV kernels; G = 128):
- *   Rows are cut into row tiles of 16 rows (M % 16 == 0), row tiles into bands of 4 tiles
- *   (64 rows; the last band holds MT % 4 tiles when MT = M/16 is not a multiple of 4).  A *unit*
- *   is (band b, group g) and is stored as ONE contiguous record of nb = tiles-in-band tiles:
- *       [nb x 256*K bytes: bit-planes][nb x 64 B: scale/bias][nb x 16 B: ratio index]
- *   Full bands come first, unit index b*NG + g (NG = N/128), each 4*(256*K + 80) bytes; the
- *   tail band's NG units follow.  Total = M*N*K/8 + 5*M*N/128 bytes (no padding).
- *   Tile i of a unit (rows 64b+16i .. +15) holds ceil(K/2) chunks; chunk q holds planes 2q and
- *   2q+1 as [lane 0..31][4 words] (the last chunk of odd K: [lane][2 words]).  Lane 4*(r%8) + c
- *   holds word c (elements 32c..32c+31 of the group) of row r%8 then of row r%8+8 of the tile:
- *   word index (t%2)*2 + (r%16)/8.  This is the A-fragment order of mma.m16n8k32 (lane =
- *   4*groupID + threadID_in_group), so a warp's 16-byte loads land in the A registers directly.
- *   scale/bias entry 2*(r%8) + (r%16)/8 of tile i = fp16 s (bits 0-15) | fp16 b (bits 16-31);
- *   ratio-index byte 2*(r%8) + (r%16)/8 of tile i = uint8 index into R.
+ *   Rows are cut into row blocks of 128 rows (M % 16 == 0; the last block holds M % 128 rows
+ *   when M is not a multiple of 128).  A *unit* is (row block rb, group g), stored as ONE
+ *   contiguous record of R = rows-in-block rows:
+ *       [R x 16K bytes: bit-planes][R x 4 B: scale/bias][R x 1 B: ratio index]
+ *   Units are ordered rb-major (unit index rb*NG + g, NG = N/128); full blocks are 128*(16K+5)
+ *   bytes each, the tail block's NG units follow.  Total = M*N*K/8 + 5*M*N/128 bytes.
+ *   Row r of a unit holds K 16-byte chunks; chunk t = words c = 0..3 of plane t (elements
+ *   32c..32c+31 of the group) and is stored at chunk position t ^ swz(r), swz(r) = (r>>2)&1 for
+ *   K = 2 or 6, (r>>1)&3 for K = 4, r&7 for K = 8, 0 otherwise (so eight consecutive rows'
+ *   16-byte loads of one plane hit eight distinct shared-memory bank groups).  One GEMV thread
+ *   owns one row = one tensor-memory lane.
+ *   scale/bias word r = fp16 s (bits 0-15) | fp16 b (bits 16-31); ratio-index byte r = uint8
+ *   index into R.
  *   ratio_pow [n_ratio][K] fp32 = r_i^t (repeated multiplication in fp64, rounded to fp32).
  *
  * Device activation layout (SBVR-x, written by sbvr_encode_vector):
@@ -76,11 +76,15 @@ typedef enum { SBVR_F32 = 0, SBVR_F16 = 1, SBVR_BF16 = 2 } sbvr_dtype;
 typedef enum { SBVR_ACT_FP16 = 0, SBVR_ACT_SBVR = 1 } sbvr_act_kind;
 
 /* GEMV algorithm selector for sbvr_gemv_ex / sbvr_debug_partials.
- *  AUTO  : the fastest implemented kernel for the activation kind (IMMA for SBVR-x).
+ *  AUTO  : the fastest implemented kernel for the activation kind and batch (SBVR-x: MMA for
+ *          T < 4, TC for T >= 4).
  *  POPC  : the paper's formulation, CUDA-core AND + __popc + coefficient FMAs.
- *  IMMA  : bit-sliced popcount on the int8 tensor pipe: (plane & 0x01010101<<s) x (d_j<<(7-s))
- *          with mma.m16n8k32.u8, which counts popc(beta_t & d_j) for 16 rows x 8 planes.   */
-typedef enum { SBVR_ALGO_AUTO = 0, SBVR_ALGO_POPC = 1, SBVR_ALGO_IMMA = 2 } sbvr_algo;
+ *  TC    : bit-sliced popcount on the 5th-generation tensor cores: A = plane & 0x01010101<<s in
+ *          tensor memory, B = d_j bit-sliced x 2^(7-s) in shared memory, tcgen05.mma kind::i8
+ *          M=128 N=8T K=32, which counts popc(beta_t & d_j) for 128 rows x 8 planes x T tokens.
+ *  MMA   : the same bit-sliced popcount with warp-level mma.sync.m16n8k32.u8 (16 rows x 8 planes
+ *          per instruction), the faster issue rate at batch 1.                                  */
+typedef enum { SBVR_ALGO_AUTO = 0, SBVR_ALGO_POPC = 1, SBVR_ALGO_TC = 2, SBVR_ALGO_MMA = 3 } sbvr_algo;
 
 /* Offline encoder knobs (SURVEY §8c.3 readings A1, A4). */
 typedef struct {
@@ -156,7 +160,7 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
                          size_t ws_bytes, int32_t algo, void* stream);
 
 /* Test-only: the integer popcount partials P[m][g][t][j] = popc(beta_t & d_j) over the group,
- * int32 [M][N/G][K][l] row-major (device), computed by the kernel `algo` (POPC or IMMA) from an
+ * int32 [M][N/G][K][l] row-major (device), computed by the kernel `algo` (POPC, TC or MMA) from an
  * SBVR-x activation (T = 1). */
 sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_t algo, int32_t* P, void* stream);
 

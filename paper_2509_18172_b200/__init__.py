@@ -25,7 +25,7 @@ _lib = None
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_ALIGNMENT, ERR_CUDA, ERR_WORKSPACE = range(7)
 F32, F16, BF16 = 0, 1, 2
 ACT_FP16, ACT_SBVR = 0, 1
-ALGO_AUTO, ALGO_POPC, ALGO_IMMA = 0, 1, 2
+ALGO_AUTO, ALGO_POPC, ALGO_TC, ALGO_MMA = 0, 1, 2, 3
 G = 128
 
 
@@ -246,7 +246,7 @@ def gemv_batched(w: SbvrWeights, X: SbvrActivation, Y: Optional[torch.Tensor] = 
     return Y
 
 
-def debug_partials(w: SbvrWeights, x: SbvrActivation, algo: int = ALGO_IMMA) -> torch.Tensor:
+def debug_partials(w: SbvrWeights, x: SbvrActivation, algo: int = ALGO_TC) -> torch.Tensor:
     P = torch.full((w.M, w.N // G, w.K, x.l), -1, dtype=torch.int32, device=w.data.device)
     wd, xd = w.desc(), x.desc()
     _check(lib().sbvr_debug_partials(ctypes.byref(wd), ctypes.byref(xd), algo, _ptr(P), _stream()),

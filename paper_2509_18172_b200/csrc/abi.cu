@@ -133,7 +133,8 @@ sbvr_status sbvr_gemv_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* 
   if (T < 1 || T > kMaxT) return set_error(SBVR_ERR_SHAPE, "T=%d outside 1..16", T);
   if (w->M <= 0 || w->N <= 0 || w->M % kTileRows || w->N % kG)
     return set_error(SBVR_ERR_SHAPE, "bad M/N %d/%d", w->M, w->N);
-  *bytes = imma_workspace_bytes(w, T);
+  const size_t a = tc_workspace_bytes(w, T), b = mma_workspace_bytes(w, T);
+  *bytes = a > b ? a : b;
   return SBVR_OK;
 }
 
@@ -154,15 +155,17 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
   if (!Y) return set_error(SBVR_ERR_INVALID_ARG, "Y is NULL");
   cudaStream_t st = (cudaStream_t)stream;
   if (X->kind == SBVR_ACT_FP16) {
-    if (algo == SBVR_ALGO_IMMA) return set_error(SBVR_ERR_UNSUPPORTED, "IMMA fp16-x kernel not built");
+    if (algo == SBVR_ALGO_TC) return set_error(SBVR_ERR_UNSUPPORTED, "tensor-memory fp16-x kernel not built");
     return launch_gemv_fp16x(w, X, T, Y, st);
   }
   if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, X, T, Y, nullptr, st);
-  if (algo != SBVR_ALGO_AUTO && algo != SBVR_ALGO_IMMA) return set_error(SBVR_ERR_INVALID_ARG, "bad algo %d", algo);
-  size_t need = imma_workspace_bytes(w, T);
+  if (algo == SBVR_ALGO_AUTO) algo = T < kTcMinT ? SBVR_ALGO_MMA : SBVR_ALGO_TC;
+  if (algo != SBVR_ALGO_TC && algo != SBVR_ALGO_MMA) return set_error(SBVR_ERR_INVALID_ARG, "bad algo %d", algo);
+  size_t need = algo == SBVR_ALGO_TC ? tc_workspace_bytes(w, T) : mma_workspace_bytes(w, T);
   if (need && (!workspace || ws_bytes < need))
     return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
-  return launch_gemv_imma(w, X, T, Y, workspace, ws_bytes, nullptr, st);
+  if (algo == SBVR_ALGO_TC) return launch_gemv_tc(w, X, T, Y, workspace, ws_bytes, nullptr, st);
+  return launch_gemv_mma(w, X, T, Y, workspace, ws_bytes, nullptr, st);
 }
 
 sbvr_status sbvr_gemv(const sbvr_weights* w, const sbvr_act* x, float* y, void* workspace, size_t ws_bytes,
@@ -183,8 +186,9 @@ sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_
   if (!P) return set_error(SBVR_ERR_INVALID_ARG, "P is NULL");
   if (x->kind != SBVR_ACT_SBVR) return set_error(SBVR_ERR_INVALID_ARG, "partials need an SBVR activation");
   if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, x, 1, nullptr, P, (cudaStream_t)stream);
-  if (algo == SBVR_ALGO_IMMA || algo == SBVR_ALGO_AUTO)
-    return launch_gemv_imma(w, x, 1, nullptr, nullptr, 0, P, (cudaStream_t)stream);
+  if (algo == SBVR_ALGO_TC) return launch_gemv_tc(w, x, 1, nullptr, nullptr, 0, P, (cudaStream_t)stream);
+  if (algo == SBVR_ALGO_MMA || algo == SBVR_ALGO_AUTO)
+    return launch_gemv_mma(w, x, 1, nullptr, nullptr, 0, P, (cudaStream_t)stream);
   return set_error(SBVR_ERR_INVALID_ARG, "bad algo %d", algo);
 }
 

@@ -1,0 +1,648 @@
+// gemv_mma.cu -- SBVR GEMV at batch 1-3 (§4.4): the AND+popcount inner
+// products on the int8 tensor pipe through warp-level mma.sync (IMMA.16832), the path with the
+// highest instruction throughput when the activation side is only l = 8 bit-planes wide.
+//
+// The paper's kernel computes, per (row, group), P_tj = popc(beta_t AND d_j) on CUDA cores and
+// then sum_t c_t sum_j alpha_j P_tj.  On B200 POPC issues at 16 lanes/clk/SM, which caps that
+// formulation near 30% of HBM bandwidth (profiles/r01_step0_microbench.jsonl); tcgen05.mma
+// kind::i8 costs a flat ~46 cycles per M=128 instruction for any N <= 64
+// (profiles/r01_tc_rate.jsonl), too slow when N = 8.  A u8 MMA whose operands are single bits IS
+// an AND+popcount: with
+//     A[row][k] = bit(beta_t, e(k)) * 2^s        (one LOP3: plane_word & (0x01010101 << s))
+//     B[k][j]   = bit(d_j,   e(k)) * 2^(7-s)     (activation plane j, built once per group)
+// every product is 128 * (beta AND d), so D[row][j] accumulated over the 128 elements of a
+// group is exactly 128 * P_tj.  One mma.m16n8k32.u8 evaluates 16 rows x 8 activation planes x
+// 32 elements = 512 weight bits (64 bytes) of AND+popcount.
+//
+// Fragment mapping (mma.m16n8k32, lane = 4*gq + c): a0/a2 = row gq, a1/a3 = row gq+8; a0/a1
+// cover k = 4c..4c+3 (bits s of the 4 bytes of word c), a2/a3 k = 16+4c.. (bits s'); four MMAs
+// with (s, s') = (0,1), (2,3), (4,5), (6,7) consume all 32 bits of each lane's word, i.e. the
+// whole 128-element group of one plane for 16 rows.  Lane (gq, c) gathers word c of its two
+// rows with LDS.32 from the row-major unit record (sbvr.h); the chunk swizzle makes the 32 lanes
+// hit 32 distinct banks.
+//
+// Data movement: a "band" is one 64-row half of a 128-row block; each warp streams its own
+// contiguous range of (band, group) units (4 KB of planes at K=4 + 320 B of metadata, three
+// cp.async.bulk copies) into a private 2-slot shared-memory ring (mbarrier complete_tx).
+//
+// Epilogue per (row, plane): lane c holds columns j = 2c, 2c+1, u = D0 + kappa*D1 (IMAD, exact,
+// kappa = alpha_{2c+1}/alpha_{2c}), converted exactly on the FMA pipe with the 1.5*2^23 magic
+// number, y += s_x * (s * sum_t r^t u_t + b * sum_t u_t) (c_t = s r^t + b, Eq. 4);
+// alpha_{2c}/128 is applied when the quad is reduced (2 shuffles per row per band).
+//
+// Work split: units are split into contiguous, balanced ranges over CTAs (8 warps each, units
+// V0 + warp + 8k).  A band shared by several CTAs is owned by its first contributor, which adds
+// the per-warp partials the later contributors published (release flags) in (CTA, warp) order:
+// deterministic, and nobody waits mid-stream.  A band with fewer than 4 row tiles (M % 64 != 0)
+// is handled by a second launch instantiated for that band height.
+#include <cstdlib>
+
+#include "sbvr_internal.cuh"
+
+namespace sbvr {
+namespace {
+
+constexpr int kImmaWarps = 16;       // warps per CTA (one CTA per SM: the register file is full)
+constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at least this many units per CTA
+constexpr int kSlots = 2;            // shared-memory ring depth per warp
+constexpr int kMaxTT = 4;            // tokens per pass (batched)
+constexpr int kBandsPerCta = 4;      // bands a CTA range may touch (host guarantees)
+constexpr int kSumBatch = 8;         // CTA partials loaded per batch by a band's last CTA
+
+struct ImmaParams {
+  const uint8_t* units;     // the weights' unit records (sbvr.h)
+  const float* ratio_pow;   // [n_ratio][K]
+  const uint32_t* xplanes;  // [T][NG][l][4]
+  const float* xscales;     // [T][NG]
+  float* Y;                 // [T][M]
+  int32_t* P;               // debug partials [M][NG][K][l]
+  float* ws_part;           // [CTA][2][TT][64] partials of a CTA's first / last band when shared
+  unsigned int* ws_cnt;     // [band] arrival counters (reset by each band's last contributor)
+  int M, N, l, n_ratio;
+  int band0;                // first band of this launch
+  int K, n_full, tail_rows; // row blocks: full ones, rows of the tail block
+  int Us;                   // units in this launch
+  int Pw, qq, rr;           // CTAs and the unit partition over CTAs
+  int one;                  // = 1 (runtime value, see i2f_fma)
+  unsigned long long* ts;   // diagnostics (env SBVR_TS_PTR): [CTA][warp][8] stamps 0-3, smid, units
+};
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TSW(slot) do { if (p.ts && lane == 0) p.ts[((size_t)blockIdx.x * kImmaWarps + wib) * 8 + (slot)] = gtime(); } while (0)
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t bslice(uint32_t X, int s) {
+  // byte b of the result = bit (8b + s) of X placed at bit (7 - s) of byte b
+  const int sh = 7 - 2 * s;
+  const uint32_t y = sh >= 0 ? (X << sh) : __umulhi(X, 1u << (32 + sh));
+  return y & (0x01010101u << (7 - s));
+}
+
+__device__ __forceinline__ void mma_u8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                       uint32_t b1, int c0, int c1, int c2, int c3) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
+}
+
+// exact int -> float for |u| < 2^22 without the ALU pipe: (u + 0x4B400000) as float - 12582912
+__device__ __forceinline__ float i2f_fma(int u, int one) {
+  int v;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(v) : "r"(u), "r"(one), "r"(0x4B400000));
+  return __int_as_float(v) - 12582912.0f;
+}
+
+__device__ __forceinline__ int imad(int a, int b, int c) {
+  int d;
+  asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+template <int K, int NB>
+struct Geom {
+  static constexpr int kTileBytes = 256 * K;
+  static constexpr int kPlaneBytes = NB * kTileBytes;
+  static constexpr int kSbBytes = NB * 64;
+  static constexpr int kRiBytes = NB * 16;
+  static constexpr int kUnitBytes = kPlaneBytes + kSbBytes + kRiBytes;
+  static constexpr int kSlotBytes = (kUnitBytes + 127) / 128 * 128;
+  static constexpr int kWarpBytes = kSlots * kSlotBytes;
+};
+
+__device__ __forceinline__ int unit_owner(int v, int qq, int rr) {
+  const int big = rr * (qq + 1);
+  return v < big ? v / (qq + 1) : rr + (v - big) / qq;
+}
+
+// a band is the half h of row block rb: its planes, scale/bias and ratio indices are three
+// contiguous pieces of the (rb, g) unit record.  Tiles [i0, i1) of the band -> three bulk copies
+// into the slot at their full-unit offsets [planes][sb][ri].
+template <int K, int NB>
+__device__ __forceinline__ void issue_unit(uint8_t* slot, uint64_t* bar, const ImmaParams& p, int band, int g,
+                                           int i0, int i1) {
+  using Gm = Geom<K, NB>;
+  const int NG = p.N / kG;
+  const int rb = band >> 1, h = band & 1;
+  const int R = rb < p.n_full ? 128 : p.tail_rows;
+  const size_t ub = (size_t)R * (16 * K + 5);
+  const uint8_t* u = rb < p.n_full ? p.units + ((size_t)rb * NG + g) * ub
+                                    : p.units + (size_t)p.n_full * NG * (128 * (16 * K + 5)) + (size_t)g * ub;
+  const int r0 = 64 * h + 16 * i0, nt = i1 - i0;
+  mbar_expect_tx(bar, nt * (Gm::kTileBytes + 64 + 16));
+  bulk_g2s(slot + i0 * Gm::kTileBytes, u + (size_t)r0 * 16 * K, nt * Gm::kTileBytes, bar);
+  bulk_g2s(slot + Gm::kPlaneBytes + 64 * i0, u + (size_t)R * 16 * K + 4 * r0, nt * 64, bar);
+  bulk_g2s(slot + Gm::kPlaneBytes + Gm::kSbBytes + 16 * i0, u + (size_t)R * (16 * K + 4) + r0, nt * 16, bar);
+}
+
+template <int K, int NB, int TT, bool DEBUG>
+__global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams p) {
+  using Gm = Geom<K, NB>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ float s_rat[64];                 // r_i (fp32) for the Horner evaluation of sum_t r^t u_t
+  __shared__ uint64_t s_bar[kImmaWarps][kSlots];
+  __shared__ unsigned int s_cnt[kBandsPerCta];  // warps done with each band of the CTA range
+  // dynamic smem: [rings][s_part: kBandsPerCta x warps x TT x 64]
+  float* s_part = reinterpret_cast<float*>(smem + kImmaWarps * Gm::kWarpBytes);
+  // let the next kernel in the stream get scheduled as soon as our CTAs retire
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int gq = lane >> 2, c = lane & 3;
+  const int NG = p.N / kG;
+  TSW(0);
+  // CTA range [V0, V1) of units (balanced to +-1 unit); its NB-tile units are split over the
+  // warps at tile granularity: warp w takes the contiguous CTA-local tiles [T0, T1)
+  const int cta = blockIdx.x;
+  const int V0 = cta * p.qq + min(cta, p.rr);
+  const int V1 = V0 + p.qq + (cta < p.rr ? 1 : 0);
+  const int bA = V0 / NG;                              // first launch-local band of this CTA
+  const int nTc = (V1 - V0) * NB;
+  const int tq = nTc / kImmaWarps, tr = nTc % kImmaWarps;
+  const int T0 = wib * tq + min(wib, tr), T1 = T0 + tq + (wib < tr ? 1 : 0);
+  const int n_mine = T1 > T0 ? (T1 - 1) / NB - T0 / NB + 1 : 0;   // units this warp touches
+  const int uf = V0 + T0 / NB;                          // its first unit
+  auto tiles_of = [&](int k, int& i0, int& i1) {        // tiles of the warp's k-th unit
+    i0 = k == 0 ? T0 % NB : 0;
+    i1 = k == n_mine - 1 ? (T1 - 1) % NB + 1 : NB;
+  };
+  uint8_t* ring = smem + wib * Gm::kWarpBytes;
+  uint64_t* bars = s_bar[wib];
+  if (n_mine > 0 && lane == 0) {
+    // weights are immutable: their TMA starts before we wait for the previous kernel
+#pragma unroll
+    for (int s2 = 0; s2 < kSlots; ++s2) mbar_init(bars + s2, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int s2 = 0; s2 < kSlots; ++s2)
+      if (s2 < n_mine) {
+        int i0, i1;
+        tiles_of(s2, i0, i1);
+        issue_unit<K, NB>(ring + s2 * Gm::kSlotBytes, bars + s2, p, p.band0 + (uf + s2) / NG, (uf + s2) % NG, i0, i1);
+      }
+  }
+  for (int i = threadIdx.x; i < p.n_ratio; i += blockDim.x) s_rat[i] = K >= 2 ? p.ratio_pow[i * K + 1] : 0.f;
+  for (int i = threadIdx.x; i < kBandsPerCta; i += blockDim.x) s_cnt[i] = 0u;
+  __syncthreads();
+  if (n_mine <= 0) return;
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // activations / workspace / y only from here
+
+  // lane constants (Eq. 12: alpha_j = 2^j, alpha_{l-1} = -2^(l-1); MMA columns j0 = 2c, j1 = 2c+1)
+  const int j0 = 2 * c, j1 = 2 * c + 1;
+  const int al0 = j0 < p.l - 1 ? (1 << j0) : (j0 == p.l - 1 ? -(1 << j0) : 0);
+  const int al1 = j1 < p.l - 1 ? (1 << j1) : (j1 == p.l - 1 ? -(1 << j1) : 0);
+  const int kappa = al0 != 0 ? al1 / al0 : 0;
+  const float lane_scale = (float)al0 * (1.0f / 128.0f);
+  // column 2c of every accumulator starts at 1.5*2^23 (as float bits): u = D0 + kappa*D1 is then
+  // the float 1.5*2^23 + 128 (P_2c + kappa P_2c+1), exact, with no int->float conversion
+  const int magic = 0x4B400000;
+  const float2 cmagic = make_float2(12582912.0f, 12582912.0f);
+  // lanes whose activation plane gq >= l contribute 0: their B words are masked at use time
+  const uint32_t xmask = gq < p.l ? 0xffffffffu : 0u;
+  const uint32_t* xlane_ptr = p.xplanes + (gq < p.l ? gq * 4 + c : 0);
+  const int xstride = p.l * 4;
+  // chunk swizzle of rows gq and gq+8 (sbvr.h; depends on the low 3 row bits only)
+  const int swz_a = chunk_swizzle(K, gq), swz_b = chunk_swizzle(K, gq + 8);
+
+  float2 acc[TT][NB];
+#pragma unroll
+  for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+    for (int i = 0; i < NB; ++i) acc[tk][i] = make_float2(0.f, 0.f);
+
+  int u = uf;
+  int b = u / NG, g = u - b * NG;
+  int slot = 0;
+  uint32_t phase = 0;
+  uint32_t Xn[TT];
+  float sxn[TT];
+#pragma unroll
+  for (int tk = 0; tk < TT; ++tk) {
+    Xn[tk] = __ldg(xlane_ptr + ((size_t)tk * NG + g) * xstride);
+    sxn[tk] = __ldg(p.xscales + (size_t)tk * NG + g);
+  }
+
+  for (int k = 0; k < n_mine; ++k) {
+    // ---- B operand for group g: activation plane gq, word c, bit-sliced and pre-scaled by 2^(7-s)
+    uint32_t Bq[TT][4][2];
+    float sx[TT];
+#pragma unroll
+    for (int tk = 0; tk < TT; ++tk) {
+      sx[tk] = sxn[tk];
+      const uint32_t X = Xn[tk] & xmask;
+#pragma unroll
+      for (int pr = 0; pr < 4; ++pr) {
+        Bq[tk][pr][0] = bslice(X, 2 * pr);
+        Bq[tk][pr][1] = bslice(X, 2 * pr + 1);
+      }
+    }
+    // next unit of this warp: band/group, activation prefetch
+    int gn = g + 1, bn = b;
+    if (gn == NG) { gn = 0; ++bn; }
+    int ti0, ti1;
+    tiles_of(k, ti0, ti1);
+    const bool has_next = k + 1 < n_mine;
+    {
+      const int gp = has_next ? gn : g;
+#pragma unroll
+      for (int tk = 0; tk < TT; ++tk) {
+        Xn[tk] = __ldg(xlane_ptr + ((size_t)tk * NG + gp) * xstride);
+        sxn[tk] = __ldg(p.xscales + (size_t)tk * NG + gp);
+      }
+    }
+
+    uint8_t* sl = ring + slot * Gm::kSlotBytes;
+    mbar_wait(bars + slot, phase);
+    if (k == 0) TSW(1);
+
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      if (i < ti0 || i >= ti1) continue;                // not this warp's tile (warp-uniform)
+      // lane (gq, c): word c of plane t of rows 16i+gq and 16i+gq+8 (row-major, chunk t at t ^ swz)
+      uint32_t w[2 * K];
+      const uint8_t* ra = sl + (16 * i + gq) * 16 * K + 4 * c;
+      const uint8_t* rb8 = ra + 8 * 16 * K;
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        w[2 * t] = *reinterpret_cast<const uint32_t*>(ra + 16 * (t ^ swz_a));
+        w[2 * t + 1] = *reinterpret_cast<const uint32_t*>(rb8 + 16 * (t ^ swz_b));
+      }
+      const uint32_t sb0 = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq) * 4);
+      const uint32_t sb1 = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq + 8) * 4);
+      const float2 r2 = make_float2(s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq]],
+                                    s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq + 8]]);
+
+      // ---- AND + popcount on the tensor pipe: K independent chains (planes) of 4 MMAs
+      int D[TT][K][4];
+#pragma unroll
+      for (int pr = 0; pr < 4; ++pr) {
+        const uint32_t m0 = 0x01010101u << (2 * pr), m1 = 0x01010101u << (2 * pr + 1);
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+          const uint32_t a0 = w[2 * t] & m0, a1 = w[2 * t + 1] & m0, a2 = w[2 * t] & m1, a3 = w[2 * t + 1] & m1;
+#pragma unroll
+          for (int tk = 0; tk < TT; ++tk) {
+            if (pr == 0)
+              mma_u8(D[tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], DEBUG ? 0 : magic, 0, DEBUG ? 0 : magic, 0);
+            else
+              mma_u8(D[tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], D[tk][t][0], D[tk][t][1],
+                     D[tk][t][2], D[tk][t][3]);
+          }
+        }
+      }
+
+      if (DEBUG) {
+        const int r0w = 64 * (p.band0 + b) + 16 * i + gq;
+#pragma unroll
+        for (int t = 0; t < K; ++t)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int32_t* dst = p.P + (((size_t)(r0w + 8 * h) * NG + g) * K + t) * p.l;
+            if (j0 < p.l) dst[j0] = D[0][t][2 * h] >> 7;
+            if (j1 < p.l) dst[j1] = D[0][t][2 * h + 1] >> 7;
+          }
+      } else {
+        const float2 s2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0 & 0xffffu))),
+                                      __half2float(__ushort_as_half((unsigned short)(sb1 & 0xffffu))));
+        const float2 b2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0 >> 16))),
+                                      __half2float(__ushort_as_half((unsigned short)(sb1 >> 16))));
+#pragma unroll
+        for (int tk = 0; tk < TT; ++tk) {
+          // f_t = 128 (P_2c + kappa P_2c+1) for rows (gq, gq+8), exact; Horner over t in fp32x2
+          float2 Ph = __fadd2_rn(make_float2(__int_as_float(imad(D[tk][K - 1][1], kappa, D[tk][K - 1][0])),
+                                             __int_as_float(imad(D[tk][K - 1][3], kappa, D[tk][K - 1][2]))),
+                                 make_float2(-cmagic.x, -cmagic.y));
+          float2 U = Ph;
+#pragma unroll
+          for (int t = K - 2; t >= 0; --t) {
+            const float2 f = __fadd2_rn(make_float2(__int_as_float(imad(D[tk][t][1], kappa, D[tk][t][0])),
+                                                    __int_as_float(imad(D[tk][t][3], kappa, D[tk][t][2]))),
+                                        make_float2(-cmagic.x, -cmagic.y));
+            Ph = __ffma2_rn(Ph, r2, f);
+            U = __fadd2_rn(U, f);
+          }
+          const float2 v = __ffma2_rn(s2, Ph, __fmul2_rn(b2, U));
+          acc[tk][i] = __ffma2_rn(make_float2(sx[tk], sx[tk]), v, acc[tk][i]);
+        }
+      }
+    }
+
+    // ---- release the slot and refill it with this warp's unit k + kSlots
+    __syncwarp();
+    if (lane == 0 && k + kSlots < n_mine) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int u2 = uf + k + kSlots;
+      int i0, i1;
+      tiles_of(k + kSlots, i0, i1);
+      issue_unit<K, NB>(sl, bars + slot, p, p.band0 + u2 / NG, u2 % NG, i0, i1);
+    }
+    if (++slot == kSlots) { slot = 0; phase ^= 1u; }
+
+    // ---- leaving band b: quad-reduce into this warp's smem slot; the CTA's last warp done with
+    // the band combines the warp slots (warp order) and writes y, or hands the CTA partial to
+    // the band's last CTA
+    if (!DEBUG && (!has_next || bn != b)) {
+      const int bl = b - bA;
+      float* sp = s_part + ((size_t)bl * kImmaWarps + wib) * (TT * 64);
+#pragma unroll
+      for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          float x0 = acc[tk][i].x * lane_scale, x1 = acc[tk][i].y * lane_scale;
+          x0 += __shfl_xor_sync(0xffffffffu, x0, 1);
+          x1 += __shfl_xor_sync(0xffffffffu, x1, 1);
+          x0 += __shfl_xor_sync(0xffffffffu, x0, 2);
+          x1 += __shfl_xor_sync(0xffffffffu, x1, 2);
+          if (c == 0) {
+            sp[tk * 64 + 16 * i + gq] = x0;
+            sp[tk * 64 + 16 * i + gq + 8] = x1;
+          }
+          acc[tk][i] = make_float2(0.f, 0.f);
+        }
+      __syncwarp();
+      unsigned int old = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        old = atomicAdd(&s_cnt[bl], 1u);
+      }
+      old = __shfl_sync(0xffffffffu, old, 0);
+      // warps of this CTA with tiles in band b: a contiguous run [wf, wl]
+      const int lo = max(V0, b * NG), hi = min(V1, (b + 1) * NG);
+      const int wf = unit_owner(NB * (lo - V0), tq, tr), wl = unit_owner(NB * (hi - V0) - 1, tq, tr);
+      const int nw = wl - wf + 1;
+      TSW(6);
+      if (old == (unsigned int)(nw - 1)) {
+        __threadfence_block();
+        const bool shared = lo > b * NG || hi < min((b + 1) * NG, p.Us);
+        float v[TT][2];
+#pragma unroll
+        for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int e = tk * 64 + lane + 32 * h;
+            float sum = 0.f;
+            for (int w2 = wf; w2 <= wl; ++w2)             // contributing warps, in warp order
+              sum += s_part[((size_t)bl * kImmaWarps + w2) * (TT * 64) + e];
+            v[tk][h] = sum;
+          }
+        if (!shared) {
+#pragma unroll
+          for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int row = lane + 32 * h;
+              if (row < 16 * NB) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
+            }
+        } else {
+          const int slotc = b == bA ? 0 : 1;
+          float* part = p.ws_part + ((size_t)cta * 2 + slotc) * (TT * 64);
+#pragma unroll
+          for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) part[tk * 64 + lane + 32 * h] = v[tk][h];
+          __syncwarp();
+          unsigned int oldg = 0;
+          if (lane == 0)                                  // release our partial, acquire the others'
+            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(oldg) : "l"(p.ws_cnt + b) : "memory");
+          oldg = __shfl_sync(0xffffffffu, oldg, 0);
+          TSW(7);
+          const int cfirst = unit_owner(b * NG, p.qq, p.rr);
+          const int clast = unit_owner(min((b + 1) * NG, p.Us) - 1, p.qq, p.rr);
+          if (oldg == (unsigned int)(clast - cfirst)) {   // last CTA of the band: sum in CTA order
+            __syncwarp();
+#pragma unroll
+            for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int e = tk * 64 + lane + 32 * h;
+                float sum = 0.f;
+                for (int cb = cfirst; cb <= clast; cb += kSumBatch) {
+                  float vals[kSumBatch];                  // all loads of a batch in flight at once
+#pragma unroll
+                  for (int j = 0; j < kSumBatch; ++j) {
+                    const int c2 = cb + j;
+                    const int V0c = c2 * p.qq + min(c2, p.rr);
+                    vals[j] = (c2 > clast || c2 == cta)
+                                  ? 0.f
+                                  : __ldcg(p.ws_part + ((size_t)c2 * 2 + (b == V0c / NG ? 0 : 1)) * (TT * 64) + e);
+                  }
+#pragma unroll
+                  for (int j = 0; j < kSumBatch; ++j)
+                    if (cb + j <= clast) sum += cb + j == cta ? v[tk][h] : vals[j];
+                }
+                const int row = lane + 32 * h;
+                if (row < 16 * NB) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = sum;
+              }
+            if (lane == 0) p.ws_cnt[b] = 0u;               // reset for the next launch
+          }
+        }
+      }
+    }
+    if (k + 1 == n_mine) TSW(2);
+    b = bn;
+    g = gn;
+    ++u;
+  }
+  TSW(3);
+  if (p.ts && lane == 0) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.ts[((size_t)blockIdx.x * kImmaWarps + wib) * 8 + 4] = smid;
+    p.ts[((size_t)blockIdx.x * kImmaWarps + wib) * 8 + 5] = n_mine;
+  }
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+struct Plan {
+  int NG, MT, n_full, tail_nb, n_bands;
+  int Us_main, C_main, Us_tail, C_tail;
+};
+
+// CTAs per launch: one per SM (16 warps; every SM gets the same work, and a CTA of the next
+// launch cannot co-reside and idle at griddepcontrol.wait while holding half an SM), at most one
+// per kMinUnitsPerCta units, and at least enough that a CTA range (<= (kBandsPerCta - 1) * NG
+// units) touches <= kBandsPerCta bands.  Nothing waits on another CTA, so more CTAs than SMs
+// are merely a second wave.
+static int ctas_for(int Us, int NG) {
+  if (Us <= 0) return 0;
+  int C = num_sms();
+  const int cap = (Us + kMinUnitsPerCta - 1) / kMinUnitsPerCta;
+  if (C > cap) C = cap;
+  const int max_range = (kBandsPerCta - 1) * NG;
+  const int need = (Us + max_range - 1) / max_range;
+  if (C < need) C = need;
+  return C < 1 ? 1 : C;
+}
+
+static Plan make_plan(const sbvr_weights* w) {
+  Plan pl;
+  pl.NG = w->N / kG;
+  pl.MT = w->M / kTileRows;
+  pl.n_full = pl.MT / 4;
+  pl.tail_nb = pl.MT % 4;
+  pl.n_bands = pl.n_full + (pl.tail_nb ? 1 : 0);
+  pl.Us_main = pl.n_full * pl.NG;
+  pl.C_main = ctas_for(pl.Us_main, pl.NG);
+  pl.Us_tail = pl.tail_nb ? pl.NG : 0;
+  pl.C_tail = ctas_for(pl.Us_tail, pl.NG);
+  return pl;
+}
+
+// workspace = [band counters: one u32 per band][partials: 2 x TT x 64 floats per CTA]
+size_t mma_workspace_bytes_(const sbvr_weights* w, int T) {
+  const Plan pl = make_plan(w);
+  const int TT = T < kMaxTT ? T : kMaxTT;
+  const int C = pl.C_main > pl.C_tail ? pl.C_main : pl.C_tail;
+  const size_t cnt = ((size_t)pl.n_bands * 4 + 255) / 256 * 256;
+  return cnt + (size_t)C * 2 * TT * 64 * sizeof(float);
+}
+
+template <int K, int NB, int TT, bool DEBUG>
+static cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
+  const int smem = kImmaWarps * Geom<K, NB>::kWarpBytes + kBandsPerCta * kImmaWarps * TT * 64 * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.Pw);
+  cfg.blockDim = dim3(kImmaWarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG>, p);
+}
+
+template <int K, int NB>
+static cudaError_t launch_nb(const ImmaParams& p, int TT, bool debug, cudaStream_t st) {
+  if (debug) return launch_one<K, NB, 1, true>(p, st);
+  switch (TT) {
+    case 1: return launch_one<K, NB, 1, false>(p, st);
+    case 2: return launch_one<K, NB, 2, false>(p, st);
+    default: return launch_one<K, NB, 4, false>(p, st);
+  }
+}
+
+template <int K>
+static cudaError_t launch_k(const ImmaParams& p, int NB, int TT, bool debug, cudaStream_t st) {
+  switch (NB) {
+    case 4: return launch_nb<K, 4>(p, TT, debug, st);
+    case 3: return launch_nb<K, 3>(p, TT, debug, st);
+    case 2: return launch_nb<K, 2>(p, TT, debug, st);
+    default: return launch_nb<K, 1>(p, TT, debug, st);
+  }
+}
+
+static cudaError_t launch_any(int K, const ImmaParams& p, int NB, int TT, bool debug, cudaStream_t st) {
+  switch (K) {
+    case 1: return launch_k<1>(p, NB, TT, debug, st);
+    case 2: return launch_k<2>(p, NB, TT, debug, st);
+    case 3: return launch_k<3>(p, NB, TT, debug, st);
+    case 4: return launch_k<4>(p, NB, TT, debug, st);
+    case 5: return launch_k<5>(p, NB, TT, debug, st);
+    case 6: return launch_k<6>(p, NB, TT, debug, st);
+    case 7: return launch_k<7>(p, NB, TT, debug, st);
+    default: return launch_k<8>(p, NB, TT, debug, st);
+  }
+}
+
+}  // namespace
+
+size_t mma_workspace_bytes(const sbvr_weights* w, int T) { return mma_workspace_bytes_(w, T); }
+
+sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
+                            int32_t* P_debug, cudaStream_t st) {
+  const Plan pl = make_plan(w);
+  ImmaParams p;
+  p.ratio_pow = w->ratio_pow;
+  p.units = w->data;
+  p.K = w->K;
+  p.n_full = w->M / kRowBlock;
+  p.tail_rows = w->M % kRowBlock;
+  p.M = w->M; p.N = w->N; p.l = x->l; p.n_ratio = w->n_ratio;
+  p.P = P_debug;
+  p.one = 1;
+  {
+    const char* tsp = getenv("SBVR_TS_PTR");
+    p.ts = tsp ? reinterpret_cast<unsigned long long*>(strtoull(tsp, nullptr, 0)) : nullptr;
+  }
+  const size_t cnt_bytes = ((size_t)pl.n_bands * 4 + 255) / 256 * 256;
+  p.ws_cnt = ws ? reinterpret_cast<unsigned int*>(ws) : nullptr;
+  p.ws_part = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + cnt_bytes) : nullptr;
+  (void)ws_bytes;
+  const uint32_t* xp = static_cast<const uint32_t*>(x->data);
+  const bool debug = P_debug != nullptr;
+  int done = 0;
+  while (done < T) {
+    const int rem = T - done;
+    const int TT = debug ? 1 : (rem >= 4 ? 4 : (rem >= 2 ? 2 : 1));
+    p.xplanes = xp + (size_t)done * pl.NG * x->l * 4;
+    p.xscales = x->scales + (size_t)done * pl.NG;
+    p.Y = Y ? Y + (size_t)done * w->M : nullptr;
+    for (int part = 0; part < 2; ++part) {
+      const int NB = part == 0 ? 4 : pl.tail_nb;
+      const int Us = part == 0 ? pl.Us_main : pl.Us_tail;
+      if (Us == 0) continue;
+      p.band0 = part == 0 ? 0 : pl.n_full;
+      p.ws_cnt = ws ? reinterpret_cast<unsigned int*>(ws) + p.band0 : nullptr;
+      p.Us = Us;
+      p.Pw = part == 0 ? pl.C_main : pl.C_tail;
+      p.qq = Us / p.Pw;
+      p.rr = Us % p.Pw;
+      cudaError_t e = launch_any(w->K, p, NB, TT, debug, st);
+      if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "gemv_mma setup: %s", cudaGetErrorString(e));
+      sbvr_status s = check_launch("gemv_mma_kernel");
+      if (s != SBVR_OK) return s;
+    }
+    if (debug) break;
+    done += TT;
+  }
+  return SBVR_OK;
+}
+
+}  // namespace sbvr

@@ -12,47 +12,52 @@ namespace sbvr {
 constexpr int kG = 128;          // group size supported by the kernels
 constexpr int kWPG = kG / 32;    // 32-bit words per plane per group
 constexpr int kTileRows = 16;    // rows per tile (mma m16)
-constexpr int kBandTiles = 4;    // tiles per band (B-operand reuse across 64 rows)
 constexpr int kMaxK = 8;
 constexpr int kMaxT = 16;
+constexpr int kTcMinT = 4;     // AUTO: batches of >= 4 tokens go to the tensor-memory kernel
 
 // ------------------------------------------------------------------ device weight layout (sbvr.h)
-// One packed buffer of "units".  A unit is (band b of up to 4 row tiles of 16 rows, group g):
-//   [nb tiles x 256*K bytes of planes][nb x 64 B scale/bias][nb x 16 B ratio index]
-// Full bands come first (unit index b*NG + g, all the same size), then the tail band (M % 64).
+// One packed buffer of "units".  A unit is (row block rb of up to 128 rows, group g) stored as
+//   [R rows x 16K bytes: row r's K plane chunks (16 B = 4 words each), chunk t at t ^ swz(r)]
+//   [R x 4 B scale/bias][R x 1 B ratio index]
+// with R = 128 for full blocks; the last block holds M % 128 rows (a multiple of 16).  Units are
+// ordered rb-major (unit index rb*NG + g), so a row block's groups are consecutive.
+constexpr int kRowBlock = 128;
+
+__host__ __device__ __forceinline__ int chunk_swizzle(int K, int r) {
+  // makes the 16-byte chunk loads of 8 consecutive rows hit 8 distinct bank groups
+  return K == 2 ? ((r >> 2) & 1) : K == 4 ? ((r >> 1) & 3) : K == 6 ? ((r >> 2) & 1) : K == 8 ? (r & 7) : 0;
+}
+
 struct Layout {
-  int M, N, K, MT, NG, n_full, tail_nb, n_bands;
+  int M, N, K, NG, n_rb, n_full, tail_rows;
   __host__ __device__ Layout(int M_, int N_, int K_) : M(M_), N(N_), K(K_) {
-    MT = M / kTileRows;
     NG = N / kG;
-    n_full = MT / kBandTiles;
-    tail_nb = MT % kBandTiles;
-    n_bands = n_full + (tail_nb ? 1 : 0);
+    n_full = M / kRowBlock;
+    tail_rows = M % kRowBlock;
+    n_rb = n_full + (tail_rows ? 1 : 0);
   }
-  __host__ __device__ long unit_bytes(int nb) const { return (long)nb * (256L * K + 80); }
-  __host__ __device__ long unit_off(int b, int g) const {
-    if (b < n_full) return ((long)b * NG + g) * unit_bytes(kBandTiles);
-    return (long)n_full * NG * unit_bytes(kBandTiles) + (long)g * unit_bytes(tail_nb);
+  __host__ __device__ int rows_in(int rb) const { return rb < n_full ? kRowBlock : tail_rows; }
+  __host__ __device__ long unit_bytes(int rows) const { return (long)rows * (16L * K + 5); }
+  __host__ __device__ long unit_off(int rb, int g) const {
+    if (rb < n_full) return ((long)rb * NG + g) * unit_bytes(kRowBlock);
+    return (long)n_full * NG * unit_bytes(kRowBlock) + (long)g * unit_bytes(tail_rows);
   }
   __host__ __device__ long total_bytes() const {
-    return (long)n_full * NG * unit_bytes(kBandTiles) + (tail_nb ? (long)NG * unit_bytes(tail_nb) : 0L);
+    return (long)n_full * NG * unit_bytes(kRowBlock) + (tail_rows ? (long)NG * unit_bytes(tail_rows) : 0L);
   }
-  __host__ __device__ int band_tiles(int b) const { return b < n_full ? kBandTiles : tail_nb; }
   // byte offset of the 32-bit word holding plane t, word c (elements 32c..32c+31) of (row, group)
   __host__ __device__ long plane_byte(int row, int g, int t, int c) const {
-    const int rt = row / kTileRows, b = rt / kBandTiles, i = rt % kBandTiles, r16 = row % kTileRows;
-    const int lane = 4 * (r16 % 8) + c, h = r16 / 8, q = t / 2;
-    const bool last_odd = (K & 1) && (q == K / 2);
-    const long base = unit_off(b, g) + (long)i * 256 * K + (long)q * 512;
-    return last_odd ? base + lane * 8 + h * 4 : base + lane * 16 + ((t % 2) * 2 + h) * 4;
+    const int rb = row / kRowBlock, r = row % kRowBlock;
+    return unit_off(rb, g) + (long)r * 16 * K + 16 * (t ^ chunk_swizzle(K, r)) + 4 * c;
   }
   __host__ __device__ long sb_byte(int row, int g) const {
-    const int rt = row / kTileRows, b = rt / kBandTiles, i = rt % kBandTiles, r16 = row % kTileRows;
-    return unit_off(b, g) + (long)band_tiles(b) * 256 * K + i * 64 + (2 * (r16 % 8) + r16 / 8) * 4;
+    const int rb = row / kRowBlock, r = row % kRowBlock;
+    return unit_off(rb, g) + (long)rows_in(rb) * 16 * K + 4 * r;
   }
   __host__ __device__ long ri_byte(int row, int g) const {
-    const int rt = row / kTileRows, b = rt / kBandTiles, i = rt % kBandTiles, r16 = row % kTileRows;
-    return unit_off(b, g) + (long)band_tiles(b) * (256L * K + 64) + i * 16 + 2 * (r16 % 8) + r16 / 8;
+    const int rb = row / kRowBlock, r = row % kRowBlock;
+    return unit_off(rb, g) + (long)rows_in(rb) * (16L * K + 4) + r;
   }
 };
 
@@ -69,8 +74,11 @@ sbvr_status launch_ratio_table(float* ratio_pow, int n_ratio, int K, cudaStream_
 sbvr_status launch_gemv_popc(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, int32_t* P_debug,
                              cudaStream_t st);
 sbvr_status launch_gemv_fp16x(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, cudaStream_t st);
-sbvr_status launch_gemv_imma(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
-                             int32_t* P_debug, cudaStream_t st);
-size_t imma_workspace_bytes(const sbvr_weights* w, int T);
+sbvr_status launch_gemv_tc(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
+                           int32_t* P_debug, cudaStream_t st);
+size_t tc_workspace_bytes(const sbvr_weights* w, int T);
+sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
+                            int32_t* P_debug, cudaStream_t st);
+size_t mma_workspace_bytes(const sbvr_weights* w, int T);
 
 }  // namespace sbvr

@@ -58,39 +58,59 @@ def test_pack_unpack_roundtrip(M, N, K):
     assert np.array_equal(np.sort(data), np.sort(src))
 
 
-def test_device_layout_is_fragment_order():
-    """Tile 0, lane 4*gq + c holds word c of rows gq, gq+8 for planes (0, 1): sbvr.h layout."""
-    M, N, K = 16, 128, 2
-    pc = np.zeros((M, 1, K, 4), np.uint32)
+def _swz(K, r):
+    # sbvr.h: chunk t of row r is stored at chunk position t ^ swz(r)
+    return {2: (r >> 2) & 1, 4: (r >> 1) & 3, 6: (r >> 2) & 1, 8: r & 7}.get(K, 0)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 6, 8])
+def test_device_layout_is_row_major_swizzled(K):
+    """Row r of a unit holds K 16-byte plane chunks, chunk t at position t ^ swz(r) (sbvr.h)."""
+    M, N = 144, 256                                  # one full 128-row block + a 16-row tail block
+    pc = np.zeros((M, 2, K, 4), np.uint32)
     for r in range(M):
+        for g in range(2):
+            for t in range(K):
+                for c in range(4):
+                    pc[r, g, t, c] = (r << 12) | (g << 8) | (t << 4) | c
+    z = np.zeros((M, 2), np.uint16)
+    data = sb.pack_host(pc, z, z, z.astype(np.uint8))
+    ub_full, ub_tail = 128 * (16 * K + 5), 16 * (16 * K + 5)
+    assert data.size == 2 * ub_full + 2 * ub_tail
+    for r in range(M):
+        rb, rr = divmod(r, 128)
+        for g in range(2):
+            base = (g * ub_full) if rb == 0 else 2 * ub_full + g * ub_tail
+            row = data[base + rr * 16 * K: base + (rr + 1) * 16 * K].view(np.uint32).reshape(K, 4)
+            for t in range(K):
+                assert row[t ^ _swz(K, rr)].tolist() == [(r << 12) | (g << 8) | (t << 4) | c for c in range(4)]
+
+
+def test_swizzle_is_bank_conflict_free():
+    """Eight consecutive rows' 16-byte loads of one plane chunk hit 8 distinct 16-byte bank groups."""
+    for K in range(1, 9):
         for t in range(K):
-            for c in range(4):
-                pc[r, 0, t, c] = (r << 16) | (t << 8) | c
-    z = np.zeros((M, 1), np.uint16)
-    pd = sb.pack_host(pc, z, z, z.astype(np.uint8)).view(np.uint32)
-    for lane in range(32):
-        gq, c = divmod(lane, 4)
-        got = pd[4 * lane:4 * lane + 4].tolist()
-        assert got == [(gq << 16) | c, ((gq + 8) << 16) | c, (gq << 16) | (1 << 8) | c, ((gq + 8) << 16) | (1 << 8) | c]
+            for r0 in range(0, 128, 8):
+                groups = {((r * 16 * K + 16 * (t ^ _swz(K, r))) // 16) % 8 for r in range(r0, r0 + 8)}
+                assert len(groups) == 8, (K, t, r0)
 
 
 def test_unit_record_layout():
-    """A unit = [4 tiles of planes][4 x 16 scale/bias][4 x 16 ratio index] (sbvr.h)."""
-    M, N, K = 64, 256, 4
+    """A unit = [R rows x 16K planes][R x 4 B scale/bias][R x 1 B ratio index] (sbvr.h)."""
+    M, N, K = 160, 256, 4
     pc = np.zeros((M, 2, K, 4), np.uint32)
     s16 = (np.arange(M * 2, dtype=np.uint16) + 1).reshape(M, 2)
     b16 = (np.arange(M * 2, dtype=np.uint16) + 1000).reshape(M, 2)
     ri = (np.arange(M * 2) % 251).astype(np.uint8).reshape(M, 2)
     data = sb.pack_host(pc, s16, b16, ri)
-    ub = 4 * (256 * K + 80)
-    for g in range(2):
-        unit = data[g * ub:(g + 1) * ub]
-        sbw = unit[4 * 256 * K:4 * 256 * K + 256].view(np.uint32)
-        rib = unit[4 * 256 * K + 256:]
-        for r in range(M):
-            i, r16 = divmod(r, 16)
-            e = 16 * i + 2 * (r16 % 8) + r16 // 8
-            assert sbw[e] == (int(s16[r, g]) | (int(b16[r, g]) << 16)) and rib[e] == ri[r, g]
+    for r in range(M):
+        rb, rr = divmod(r, 128)
+        R = 128 if rb == 0 else M - 128
+        for g in range(2):
+            base = g * 128 * (16 * K + 5) if rb == 0 else 2 * 128 * (16 * K + 5) + g * R * (16 * K + 5)
+            sbw = data[base + R * 16 * K: base + R * (16 * K + 4)].view(np.uint32)
+            rib = data[base + R * (16 * K + 4): base + R * (16 * K + 5)]
+            assert sbw[rr] == (int(s16[r, g]) | (int(b16[r, g]) << 16)) and rib[rr] == ri[r, g]
 
 
 def test_algorithmic_bytes_match_survey_table():

@@ -101,12 +101,12 @@ def test_encode_weights_deterministic():
 
 
 # ------------------------------------------------------------------ a5/a7: SBVR-x GEMV (partials bit-exact, y to 1e-3)
-SHAPES = [(16, 128), (64, 256), (80, 384), (208, 1024), (1024, 512)]
+SHAPES = [(16, 128), (64, 256), (80, 384), (208, 1024), (1024, 512), (336, 640), (272, 256)]
 
 
 @pytest.mark.parametrize("M,N", SHAPES)
 @pytest.mark.parametrize("K", [2, 3, 4])
-@pytest.mark.parametrize("algo", [sb.ALGO_IMMA, sb.ALGO_POPC])
+@pytest.mark.parametrize("algo", [sb.ALGO_MMA, sb.ALGO_TC, sb.ALGO_POPC])
 def test_gemv_sbvr_x(M, N, K, algo):
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=M * 7 + N + K)
     w = sb.pack_canonical(pc, s16, b16, ri, 16)
@@ -124,14 +124,15 @@ def test_gemv_sbvr_x(M, N, K, algo):
 
 
 @pytest.mark.parametrize("l", [8, 6, 5, 4, 2])
-def test_gemv_sbvr_x_activation_bits(l):
+@pytest.mark.parametrize("algo", [sb.ALGO_MMA, sb.ALGO_TC])
+def test_gemv_sbvr_x_activation_bits(l, algo):
     M, N, K = 48, 256, 4
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=l)
     w = sb.pack_canonical(pc, s16, b16, ri, 16)
     x = synthetic.activation(N, seed=l)
     act = sb.encode_vector(torch.from_numpy(x).to(DEV), l=l)
-    y = sb.gemv(w, act)
-    P = sb.debug_partials(w, act, algo=sb.ALGO_IMMA)
+    y = sb.gemv_ex(w, act, algo=algo)
+    P = sb.debug_partials(w, act, algo=algo)
     torch.cuda.synchronize()
     z, xp, sc = oracle.encode_vector(x[0], 128, l)
     enc = _oracle_encoded(pc, s16, b16, ri, K, 16)
@@ -171,13 +172,14 @@ def test_gemv_fp16_x(M, N, K):
 
 # ------------------------------------------------------------------ a8: batched
 @pytest.mark.parametrize("T", [1, 2, 3, 4, 5, 8, 16])
-def test_gemv_batched(T):
+@pytest.mark.parametrize("algo", [sb.ALGO_AUTO, sb.ALGO_MMA, sb.ALGO_TC])
+def test_gemv_batched(T, algo):
     M, N, K = 208, 512, 4
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=T)
     w = sb.pack_canonical(pc, s16, b16, ri, 16)
     X = synthetic.activation(N, seed=T + 50, T=T)
     act = sb.encode_vector(torch.from_numpy(X).to(DEV))
-    Y = sb.gemv_batched(w, act)
+    Y = sb.gemv_ex(w, act, algo=algo)
     Yf = sb.gemv_ex(w, sb.fp16_activation(torch.from_numpy(X).to(DEV)))
     torch.cuda.synchronize()
     enc = _oracle_encoded(pc, s16, b16, ri, K, 16)
@@ -189,15 +191,16 @@ def test_gemv_batched(T):
 
 # ------------------------------------------------------------------ full-size shapes, sampled rows, bench launch config
 @pytest.mark.parametrize("name,M,N", synthetic.LLAMA3_8B_LAYER + [("70b_down", 8192, 28672)])
-def test_gemv_full_size_sampled_rows(name, M, N):
+@pytest.mark.parametrize("algo", [sb.ALGO_MMA, sb.ALGO_TC])
+def test_gemv_full_size_sampled_rows(name, M, N, algo):
     K = 4
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=M ^ N)
     w = sb.pack_canonical(pc, s16, b16, ri, 16)
     x = synthetic.activation(N, seed=11)
     act = sb.encode_vector(torch.from_numpy(x).to(DEV))
     ws = sb.Workspace.for_weights(w, 1)
-    y = sb.gemv(w, act, ws=ws)
-    y2 = sb.gemv(w, act, ws=ws)              # workspace reuse: counters must have been reset
+    y = sb.gemv_ex(w, act, ws=ws, algo=algo)[0]
+    y2 = sb.gemv_ex(w, act, ws=ws, algo=algo)[0]   # workspace reuse: counters must have been reset
     torch.cuda.synchronize()
     rows = np.unique(np.concatenate([np.random.default_rng(1).choice(M, 200, replace=False), [0, M - 1, 63, 64]]))
     z, xp, sc = oracle.encode_vector(x[0], 128, 8)
@@ -206,7 +209,7 @@ def test_gemv_full_size_sampled_rows(name, M, N):
     yy = y.cpu().numpy()
     assert_close(yy[rows], ref)
     assert torch.equal(y, y2)                # deterministic
-    P = sb.debug_partials(w, act, algo=sb.ALGO_IMMA)
+    P = sb.debug_partials(w, act, algo=algo)
     Pref, _ = oracle.partials_rows(enc, z, xp, rows=rows[:16])
     assert np.array_equal(P.cpu().numpy()[rows[:16]], Pref)
 

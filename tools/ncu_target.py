@@ -14,7 +14,7 @@ ap.add_argument("--M", type=int, default=14336)
 ap.add_argument("--N", type=int, default=4096)
 ap.add_argument("--K", type=int, default=4)
 ap.add_argument("--iters", type=int, default=6)
-ap.add_argument("--algo", type=int, default=sb.ALGO_IMMA)
+ap.add_argument("--algo", type=int, default=sb.ALGO_MMA)
 ap.add_argument("--fp16x", action="store_true")
 a = ap.parse_args()
 pc, s16, b16, ri = synthetic.random_encoded(a.M, a.N, a.K, 16, seed=5)
