@@ -59,9 +59,10 @@ def lib():
     """Load libsbvr.so (building it in-tree with nvcc if it is missing or stale)."""
     global _lib
     if _lib is None:
-        if not _build.up_to_date():
+        ab = os.environ.get("SBVR_LIB_AB")          # A/B timing of an alternative build (tools/ only)
+        if not ab and not _build.up_to_date():
             _build.build()
-        L = ctypes.CDLL(_build.LIB)
+        L = ctypes.CDLL(ab or _build.LIB)
         P, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
         L.sbvr_abi_version.restype = i32
         L.sbvr_status_string.restype = ctypes.c_char_p

@@ -46,7 +46,6 @@ constexpr int kImmaWarps = 16;       // warps per CTA (one CTA per SM: the regis
 constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at least this many units per CTA
 constexpr int kSlots = 2;            // shared-memory ring depth per warp
 constexpr int kMaxTT = 4;            // tokens per pass (batched)
-constexpr int kBandsPerCta = 4;      // bands a CTA range may touch (host guarantees)
 constexpr int kSumBatch = 8;         // CTA partials loaded per batch by a band's last CTA
 
 struct ImmaParams {
@@ -170,8 +169,10 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float s_rat[64];                 // r_i (fp32) for the Horner evaluation of sum_t r^t u_t
   __shared__ uint64_t s_bar[kImmaWarps][kSlots];
-  __shared__ unsigned int s_cnt[kBandsPerCta];  // warps done with each band of the CTA range
-  // dynamic smem: [rings][s_part: kBandsPerCta x warps x TT x 64]
+  __shared__ unsigned int s_cnt[2 * kImmaWarps];  // warps done with a band, by (first warp, its first/last band)
+  __shared__ int s_fb[kImmaWarps];                 // first launch-local band of each warp
+  __shared__ int s_lb[kImmaWarps];                 // last launch-local band of each warp (-1: no tiles)
+  // dynamic smem: [rings][s_part: warps x 2 (first / last band) x TT x 64]
   float* s_part = reinterpret_cast<float*>(smem + kImmaWarps * Gm::kWarpBytes);
   // let the next kernel in the stream get scheduled as soon as our CTAs retire
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -210,7 +211,13 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
       }
   }
   for (int i = threadIdx.x; i < p.n_ratio; i += blockDim.x) s_rat[i] = K >= 2 ? p.ratio_pow[i * K + 1] : 0.f;
-  for (int i = threadIdx.x; i < kBandsPerCta; i += blockDim.x) s_cnt[i] = 0u;
+  for (int i = threadIdx.x; i < 2 * kImmaWarps; i += blockDim.x) s_cnt[i] = 0u;
+  if (threadIdx.x < kImmaWarps) {
+    const int w2 = threadIdx.x;
+    const int t0 = w2 * tq + min(w2, tr), t1 = t0 + tq + (w2 < tr ? 1 : 0);
+    s_fb[w2] = t1 > t0 ? (V0 + t0 / NB) / NG : 0x7fffffff;
+    s_lb[w2] = t1 > t0 ? (V0 + (t1 - 1) / NB) / NG : -1;
+  }
   __syncthreads();
   if (n_mine <= 0) return;
   asm volatile("griddepcontrol.wait;" ::: "memory");   // activations / workspace / y only from here
@@ -366,12 +373,19 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     }
     if (++slot == kSlots) { slot = 0; phase ^= 1u; }
 
-    // ---- leaving band b: quad-reduce into this warp's smem slot; the CTA's last warp done with
-    // the band combines the warp slots (warp order) and writes y, or hands the CTA partial to
-    // the band's last CTA
+    // ---- leaving band b.  Only a warp's first and last band can be shared with other warps of
+    // the CTA, and only a CTA's first and last band with other CTAs.  The warp parks its
+    // quad-reduced partial in its smem slot (first / last band); the last warp of the CTA done
+    // with the band (smem counter) sums the slots in warp order, then writes y or hands the CTA
+    // partial to the band's last CTA.
     if (!DEBUG && (!has_next || bn != b)) {
-      const int bl = b - bA;
-      float* sp = s_part + ((size_t)bl * kImmaWarps + wib) * (TT * 64);
+      // warps of this CTA with tiles in band b: a contiguous run [wf, wl] (ballot over the warps)
+      const unsigned int holders =
+          __ballot_sync(0xffffffffu, lane < kImmaWarps && s_fb[lane & (kImmaWarps - 1)] <= b &&
+                                         s_lb[lane & (kImmaWarps - 1)] >= b);
+      const int wf = __ffs(holders) - 1, wl = 31 - __clz(holders);
+      const bool shared = V0 > b * NG || V1 < min((b + 1) * NG, p.Us);    // other CTAs hold units of b
+      float* sp = s_part + ((size_t)wib * 2 + (b == s_fb[wib] ? 0 : 1)) * (TT * 64);
 #pragma unroll
       for (int tk = 0; tk < TT; ++tk)
 #pragma unroll
@@ -387,21 +401,22 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
           }
           acc[tk][i] = make_float2(0.f, 0.f);
         }
-      __syncwarp();
-      unsigned int old = 0;
-      if (lane == 0) {
-        __threadfence_block();
-        old = atomicAdd(&s_cnt[bl], 1u);
+      bool last = true;
+      if (wf != wl) {
+        __syncwarp();
+        unsigned int old = 0;
+        const int fbf = s_fb[wf];
+        if (lane == 0) {
+          __threadfence_block();
+          old = atomicAdd(&s_cnt[wf * 2 + (b == fbf ? 0 : 1)], 1u);
+        }
+        old = __shfl_sync(0xffffffffu, old, 0);
+        last = old == (unsigned int)(wl - wf);
       }
-      old = __shfl_sync(0xffffffffu, old, 0);
-      // warps of this CTA with tiles in band b: a contiguous run [wf, wl]
-      const int lo = max(V0, b * NG), hi = min(V1, (b + 1) * NG);
-      const int wf = unit_owner(NB * (lo - V0), tq, tr), wl = unit_owner(NB * (hi - V0) - 1, tq, tr);
-      const int nw = wl - wf + 1;
       TSW(6);
-      if (old == (unsigned int)(nw - 1)) {
+      if (last) {
+        __syncwarp();
         __threadfence_block();
-        const bool shared = lo > b * NG || hi < min((b + 1) * NG, p.Us);
         float v[TT][2];
 #pragma unroll
         for (int tk = 0; tk < TT; ++tk)
@@ -409,8 +424,8 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
           for (int h = 0; h < 2; ++h) {
             const int e = tk * 64 + lane + 32 * h;
             float sum = 0.f;
-            for (int w2 = wf; w2 <= wl; ++w2)             // contributing warps, in warp order
-              sum += s_part[((size_t)bl * kImmaWarps + w2) * (TT * 64) + e];
+            for (int w2 = wf; w2 <= wl; ++w2)               // contributing warps, in warp order
+              sum += s_part[((size_t)w2 * 2 + (b == s_fb[w2] ? 0 : 1)) * (TT * 64) + e];
             v[tk][h] = sum;
           }
         if (!shared) {
@@ -498,17 +513,12 @@ struct Plan {
 
 // CTAs per launch: one per SM (16 warps; every SM gets the same work, and a CTA of the next
 // launch cannot co-reside and idle at griddepcontrol.wait while holding half an SM), at most one
-// per kMinUnitsPerCta units, and at least enough that a CTA range (<= (kBandsPerCta - 1) * NG
-// units) touches <= kBandsPerCta bands.  Nothing waits on another CTA, so more CTAs than SMs
-// are merely a second wave.
+// per kMinUnitsPerCta units.
 static int ctas_for(int Us, int NG) {
   if (Us <= 0) return 0;
   int C = num_sms();
   const int cap = (Us + kMinUnitsPerCta - 1) / kMinUnitsPerCta;
   if (C > cap) C = cap;
-  const int max_range = (kBandsPerCta - 1) * NG;
-  const int need = (Us + max_range - 1) / max_range;
-  if (C < need) C = need;
   return C < 1 ? 1 : C;
 }
 
@@ -537,7 +547,7 @@ size_t mma_workspace_bytes_(const sbvr_weights* w, int T) {
 
 template <int K, int NB, int TT, bool DEBUG>
 static cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
-  const int smem = kImmaWarps * Geom<K, NB>::kWarpBytes + kBandsPerCta * kImmaWarps * TT * 64 * 4;
+  const int smem = kImmaWarps * Geom<K, NB>::kWarpBytes + kImmaWarps * 2 * TT * 64 * 4;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG>,

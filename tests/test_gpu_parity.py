@@ -190,7 +190,9 @@ def test_gemv_batched(T, algo):
 
 
 # ------------------------------------------------------------------ full-size shapes, sampled rows, bench launch config
-@pytest.mark.parametrize("name,M,N", synthetic.LLAMA3_8B_LAYER + [("70b_down", 8192, 28672)])
+@pytest.mark.parametrize("name,M,N", synthetic.LLAMA3_8B_LAYER + [("70b_down", 8192, 28672),
+                                                                   ("gate_up_fused", 28672, 4096),
+                                                                   ("tall_narrow", 16384, 256)])
 @pytest.mark.parametrize("algo", [sb.ALGO_MMA, sb.ALGO_TC])
 def test_gemv_full_size_sampled_rows(name, M, N, algo):
     K = 4
