@@ -138,9 +138,11 @@ sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, in
 sbvr_status sbvr_encode_vector(const uint16_t* x, int32_t T, int32_t N, int32_t group_size, int32_t l,
                                uint32_t* planes_out, float* scales_out, void* stream);
 
-/* Workspace for the GEMV kernels (split-row fix-up slots and counters).  The first use of a
- * workspace requires it zeroed (sbvr_workspace_init); kernels leave it zeroed again.  One
- * workspace must not be used by two GEMVs running concurrently on different streams. */
+/* Workspace for the GEMV kernels (cross-CTA partial-sum slots and flags for row blocks split
+ * over several CTAs).  Before its first use a workspace must be initialised with
+ * sbvr_workspace_init (fills it with 0xFF bytes: "slot empty / flag clear"); every GEMV leaves
+ * it in that state again.  One workspace must not be used by two GEMVs running concurrently on
+ * different streams. */
 sbvr_status sbvr_gemv_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* bytes);
 sbvr_status sbvr_workspace_init(void* workspace, size_t bytes, void* stream);
 

@@ -193,11 +193,13 @@ def fp16_activation(x: torch.Tensor) -> SbvrActivation:
 
 # ------------------------------------------------------------------ GEMV
 class Workspace:
-    """Caller-owned GEMV workspace (zeroed once; kernels leave it zeroed)."""
+    """Caller-owned GEMV workspace, initialised once by sbvr_workspace_init (kernels leave it in that
+    state: publish slots re-armed, flags cleared)."""
 
     def __init__(self, nbytes: int, device="cuda"):
         self.nbytes = max(int(nbytes), 256)
-        self.buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
+        self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        _check(lib().sbvr_workspace_init(_ptr(self.buf), self.nbytes, _stream()), "sbvr_workspace_init")
 
     @staticmethod
     def for_weights(w: SbvrWeights, T: int = 16) -> "Workspace":

@@ -141,7 +141,7 @@ sbvr_status sbvr_gemv_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* 
 sbvr_status sbvr_workspace_init(void* workspace, size_t bytes, void* stream) {
   if (!workspace && bytes) return set_error(SBVR_ERR_INVALID_ARG, "workspace is NULL");
   if (bytes == 0) return SBVR_OK;
-  cudaError_t e = cudaMemsetAsync(workspace, 0, bytes, (cudaStream_t)stream);
+  cudaError_t e = cudaMemsetAsync(workspace, 0xFF, bytes, (cudaStream_t)stream);
   if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
   return SBVR_OK;
 }

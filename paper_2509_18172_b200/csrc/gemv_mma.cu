@@ -46,7 +46,8 @@ constexpr int kImmaWarps = 16;       // warps per CTA (one CTA per SM: the regis
 constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at least this many units per CTA
 constexpr int kSlots = 2;            // shared-memory ring depth per warp
 constexpr int kMaxTT = 4;            // tokens per pass (batched)
-constexpr int kSumBatch = 8;         // CTA partials loaded per batch by a band's last CTA
+constexpr int kSumBatch = 8;         // CTA partials loaded per batch by a band's owner
+constexpr unsigned int kSentinel = 0xFFFFFFFFu;   // "not yet written" (a NaN arithmetic never produces)
 
 struct ImmaParams {
   const uint8_t* units;     // the weights' unit records (sbvr.h)
@@ -55,14 +56,17 @@ struct ImmaParams {
   const float* xscales;     // [T][NG]
   float* Y;                 // [T][M]
   int32_t* P;               // debug partials [M][NG][K][l]
-  float* ws_part;           // [CTA][2][TT][64] partials of a CTA's first / last band when shared
-  unsigned int* ws_cnt;     // [band] arrival counters (reset by each band's last contributor)
+  float* ws_part;           // [CTA][TT][64] partial of a CTA's first band when an earlier CTA owns it;
+                            // kSentinel words until written (sbvr_workspace_init, re-armed by the owner)
   int M, N, l, n_ratio;
   int band0;                // first band of this launch
   int K, n_full, tail_rows; // row blocks: full ones, rows of the tail block
   int Us;                   // units in this launch
   int Pw, qq, rr;           // CTAs and the unit partition over CTAs
   int one;                  // = 1 (runtime value, see i2f_fma)
+  int exp;                  // ablation bits (env SBVR_EXP_MODE, 0 in production): 1 skip the tile
+                            // compute, 2 compute only (no TMA: stale shared memory), 4 skip the
+                            // band flush, 8 exit right after the prologue
   unsigned long long* ts;   // diagnostics (env SBVR_TS_PTR): [CTA][warp][8] stamps 0-3, smid, units
 };
 __device__ __forceinline__ unsigned long long gtime() {
@@ -138,6 +142,12 @@ struct Geom {
   static constexpr int kWarpBytes = kSlots * kSlotBytes;
 };
 
+__device__ __forceinline__ uint32_t ld_relaxed(const float* ptr) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int unit_owner(int v, int qq, int rr) {
   const int big = rr * (qq + 1);
   return v < big ? v / (qq + 1) : rr + (v - big) / qq;
@@ -166,6 +176,7 @@ __device__ __forceinline__ void issue_unit(uint8_t* slot, uint64_t* bar, const I
 template <int K, int NB, int TT, bool DEBUG>
 __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams p) {
   using Gm = Geom<K, NB>;
+  constexpr int PT = (NB % 2 == 0 && TT == 1) ? 2 : 1;   // tiles per compute step
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float s_rat[64];                 // r_i (fp32) for the Horner evaluation of sum_t r^t u_t
   __shared__ uint64_t s_bar[kImmaWarps][kSlots];
@@ -186,9 +197,10 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   const int V0 = cta * p.qq + min(cta, p.rr);
   const int V1 = V0 + p.qq + (cta < p.rr ? 1 : 0);
   const int bA = V0 / NG;                              // first launch-local band of this CTA
-  const int nTc = (V1 - V0) * NB;
+  // (in steps of PT tiles: PT = 2 for even NB at batch 1, see the compute loop)
+  const int nTc = (V1 - V0) * NB / PT;
   const int tq = nTc / kImmaWarps, tr = nTc % kImmaWarps;
-  const int T0 = wib * tq + min(wib, tr), T1 = T0 + tq + (wib < tr ? 1 : 0);
+  const int T0 = PT * (wib * tq + min(wib, tr)), T1 = T0 + PT * (tq + (wib < tr ? 1 : 0));
   const int n_mine = T1 > T0 ? (T1 - 1) / NB - T0 / NB + 1 : 0;   // units this warp touches
   const int uf = V0 + T0 / NB;                          // its first unit
   auto tiles_of = [&](int k, int& i0, int& i1) {        // tiles of the warp's k-th unit
@@ -204,7 +216,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
     for (int s2 = 0; s2 < kSlots; ++s2)
-      if (s2 < n_mine) {
+      if (s2 < n_mine && !(p.exp & 2)) {
         int i0, i1;
         tiles_of(s2, i0, i1);
         issue_unit<K, NB>(ring + s2 * Gm::kSlotBytes, bars + s2, p, p.band0 + (uf + s2) / NG, (uf + s2) % NG, i0, i1);
@@ -214,13 +226,14 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   for (int i = threadIdx.x; i < 2 * kImmaWarps; i += blockDim.x) s_cnt[i] = 0u;
   if (threadIdx.x < kImmaWarps) {
     const int w2 = threadIdx.x;
-    const int t0 = w2 * tq + min(w2, tr), t1 = t0 + tq + (w2 < tr ? 1 : 0);
+    const int t0 = PT * (w2 * tq + min(w2, tr)), t1 = t0 + PT * (tq + (w2 < tr ? 1 : 0));
     s_fb[w2] = t1 > t0 ? (V0 + t0 / NB) / NG : 0x7fffffff;
     s_lb[w2] = t1 > t0 ? (V0 + (t1 - 1) / NB) / NG : -1;
   }
   __syncthreads();
   if (n_mine <= 0) return;
   asm volatile("griddepcontrol.wait;" ::: "memory");   // activations / workspace / y only from here
+  if (p.exp & 8) return;
 
   // lane constants (Eq. 12: alpha_j = 2^j, alpha_{l-1} = -2^(l-1); MMA columns j0 = 2c, j1 = 2c+1)
   const int j0 = 2 * c, j1 = 2 * c + 1;
@@ -287,84 +300,100 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     }
 
     uint8_t* sl = ring + slot * Gm::kSlotBytes;
-    mbar_wait(bars + slot, phase);
+    if (!(p.exp & 2)) mbar_wait(bars + slot, phase);
     if (k == 0) TSW(1);
 
+    // tiles are processed PT at a time so 4K independent MMA chains hide the IMMA latency; warp
+    // tile ranges are PT-aligned, so a step's tiles are all in or all out of this warp's range
 #pragma unroll
-    for (int i = 0; i < NB; ++i) {
-      if (i < ti0 || i >= ti1) continue;                // not this warp's tile (warp-uniform)
+    for (int ib = 0; ib < NB; ib += PT) {
+      if (ib < ti0 || ib >= ti1 || (p.exp & 1)) continue;   // not this warp's tiles (warp-uniform)
       // lane (gq, c): word c of plane t of rows 16i+gq and 16i+gq+8 (row-major, chunk t at t ^ swz)
-      uint32_t w[2 * K];
-      const uint8_t* ra = sl + (16 * i + gq) * 16 * K + 4 * c;
-      const uint8_t* rb8 = ra + 8 * 16 * K;
+      uint32_t w[PT][2 * K];
+      uint32_t sb0[PT], sb1[PT];
+      float2 r2[PT];
 #pragma unroll
-      for (int t = 0; t < K; ++t) {
-        w[2 * t] = *reinterpret_cast<const uint32_t*>(ra + 16 * (t ^ swz_a));
-        w[2 * t + 1] = *reinterpret_cast<const uint32_t*>(rb8 + 16 * (t ^ swz_b));
+      for (int j = 0; j < PT; ++j) {
+        const int i = ib + j;
+        const uint8_t* ra = sl + (16 * i + gq) * 16 * K + 4 * c;
+        const uint8_t* rb8 = ra + 8 * 16 * K;
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+          w[j][2 * t] = *reinterpret_cast<const uint32_t*>(ra + 16 * (t ^ swz_a));
+          w[j][2 * t + 1] = *reinterpret_cast<const uint32_t*>(rb8 + 16 * (t ^ swz_b));
+        }
+        sb0[j] = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq) * 4);
+        sb1[j] = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq + 8) * 4);
+        r2[j] = make_float2(s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq]],
+                            s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq + 8]]);
       }
-      const uint32_t sb0 = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq) * 4);
-      const uint32_t sb1 = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq + 8) * 4);
-      const float2 r2 = make_float2(s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq]],
-                                    s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq + 8]]);
 
-      // ---- AND + popcount on the tensor pipe: K independent chains (planes) of 4 MMAs
-      int D[TT][K][4];
+      // ---- AND + popcount on the tensor pipe: PT x K independent chains (tile, plane) of 4 MMAs
+      int D[PT][TT][K][4];
 #pragma unroll
       for (int pr = 0; pr < 4; ++pr) {
         const uint32_t m0 = 0x01010101u << (2 * pr), m1 = 0x01010101u << (2 * pr + 1);
 #pragma unroll
-        for (int t = 0; t < K; ++t) {
-          const uint32_t a0 = w[2 * t] & m0, a1 = w[2 * t + 1] & m0, a2 = w[2 * t] & m1, a3 = w[2 * t + 1] & m1;
-#pragma unroll
-          for (int tk = 0; tk < TT; ++tk) {
-            if (pr == 0)
-              mma_u8(D[tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], DEBUG ? 0 : magic, 0, DEBUG ? 0 : magic, 0);
-            else
-              mma_u8(D[tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], D[tk][t][0], D[tk][t][1],
-                     D[tk][t][2], D[tk][t][3]);
-          }
-        }
-      }
-
-      if (DEBUG) {
-        const int r0w = 64 * (p.band0 + b) + 16 * i + gq;
-#pragma unroll
         for (int t = 0; t < K; ++t)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            int32_t* dst = p.P + (((size_t)(r0w + 8 * h) * NG + g) * K + t) * p.l;
-            if (j0 < p.l) dst[j0] = D[0][t][2 * h] >> 7;
-            if (j1 < p.l) dst[j1] = D[0][t][2 * h + 1] >> 7;
-          }
-      } else {
-        const float2 s2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0 & 0xffffu))),
-                                      __half2float(__ushort_as_half((unsigned short)(sb1 & 0xffffu))));
-        const float2 b2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0 >> 16))),
-                                      __half2float(__ushort_as_half((unsigned short)(sb1 >> 16))));
+          for (int j = 0; j < PT; ++j) {
+            const uint32_t a0 = w[j][2 * t] & m0, a1 = w[j][2 * t + 1] & m0;
+            const uint32_t a2 = w[j][2 * t] & m1, a3 = w[j][2 * t + 1] & m1;
 #pragma unroll
-        for (int tk = 0; tk < TT; ++tk) {
-          // f_t = 128 (P_2c + kappa P_2c+1) for rows (gq, gq+8), exact; Horner over t in fp32x2
-          float2 Ph = __fadd2_rn(make_float2(__int_as_float(imad(D[tk][K - 1][1], kappa, D[tk][K - 1][0])),
-                                             __int_as_float(imad(D[tk][K - 1][3], kappa, D[tk][K - 1][2]))),
-                                 make_float2(-cmagic.x, -cmagic.y));
-          float2 U = Ph;
-#pragma unroll
-          for (int t = K - 2; t >= 0; --t) {
-            const float2 f = __fadd2_rn(make_float2(__int_as_float(imad(D[tk][t][1], kappa, D[tk][t][0])),
-                                                    __int_as_float(imad(D[tk][t][3], kappa, D[tk][t][2]))),
-                                        make_float2(-cmagic.x, -cmagic.y));
-            Ph = __ffma2_rn(Ph, r2, f);
-            U = __fadd2_rn(U, f);
+            for (int tk = 0; tk < TT; ++tk) {
+              if (pr == 0)
+                mma_u8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], DEBUG ? 0 : magic, 0,
+                       DEBUG ? 0 : magic, 0);
+              else
+                mma_u8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], D[j][tk][t][0], D[j][tk][t][1],
+                       D[j][tk][t][2], D[j][tk][t][3]);
+            }
           }
-          const float2 v = __ffma2_rn(s2, Ph, __fmul2_rn(b2, U));
-          acc[tk][i] = __ffma2_rn(make_float2(sx[tk], sx[tk]), v, acc[tk][i]);
+      }
+
+#pragma unroll
+      for (int j = 0; j < PT; ++j) {
+        const int i = ib + j;
+        if (DEBUG) {
+          const int r0w = 64 * (p.band0 + b) + 16 * i + gq;
+#pragma unroll
+          for (int t = 0; t < K; ++t)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              int32_t* dst = p.P + (((size_t)(r0w + 8 * h) * NG + g) * K + t) * p.l;
+              if (j0 < p.l) dst[j0] = D[j][0][t][2 * h] >> 7;
+              if (j1 < p.l) dst[j1] = D[j][0][t][2 * h + 1] >> 7;
+            }
+        } else {
+          const float2 s2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0[j] & 0xffffu))),
+                                        __half2float(__ushort_as_half((unsigned short)(sb1[j] & 0xffffu))));
+          const float2 b2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0[j] >> 16))),
+                                        __half2float(__ushort_as_half((unsigned short)(sb1[j] >> 16))));
+#pragma unroll
+          for (int tk = 0; tk < TT; ++tk) {
+            // f_t = 128 (P_2c + kappa P_2c+1) for rows (gq, gq+8), exact; Horner over t in fp32x2
+            float2 Ph = __fadd2_rn(make_float2(__int_as_float(imad(D[j][tk][K - 1][1], kappa, D[j][tk][K - 1][0])),
+                                               __int_as_float(imad(D[j][tk][K - 1][3], kappa, D[j][tk][K - 1][2]))),
+                                   make_float2(-cmagic.x, -cmagic.y));
+            float2 U = Ph;
+#pragma unroll
+            for (int t = K - 2; t >= 0; --t) {
+              const float2 f = __fadd2_rn(make_float2(__int_as_float(imad(D[j][tk][t][1], kappa, D[j][tk][t][0])),
+                                                      __int_as_float(imad(D[j][tk][t][3], kappa, D[j][tk][t][2]))),
+                                          make_float2(-cmagic.x, -cmagic.y));
+              Ph = __ffma2_rn(Ph, r2[j], f);
+              U = __fadd2_rn(U, f);
+            }
+            const float2 v = __ffma2_rn(s2, Ph, __fmul2_rn(b2, U));
+            acc[tk][i] = __ffma2_rn(make_float2(sx[tk], sx[tk]), v, acc[tk][i]);
+          }
         }
       }
     }
 
     // ---- release the slot and refill it with this warp's unit k + kSlots
     __syncwarp();
-    if (lane == 0 && k + kSlots < n_mine) {
+    if (lane == 0 && k + kSlots < n_mine && !(p.exp & 2)) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const int u2 = uf + k + kSlots;
       int i0, i1;
@@ -378,7 +407,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     // quad-reduced partial in its smem slot (first / last band); the last warp of the CTA done
     // with the band (smem counter) sums the slots in warp order, then writes y or hands the CTA
     // partial to the band's last CTA.
-    if (!DEBUG && (!has_next || bn != b)) {
+    if (!DEBUG && (!has_next || bn != b) && !(p.exp & 4)) {
       // warps of this CTA with tiles in band b: a contiguous run [wf, wl] (ballot over the warps)
       const unsigned int holders =
           __ballot_sync(0xffffffffu, lane < kImmaWarps && s_fb[lane & (kImmaWarps - 1)] <= b &&
@@ -437,46 +466,60 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
               if (row < 16 * NB) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
             }
         } else {
-          const int slotc = b == bA ? 0 : 1;
-          float* part = p.ws_part + ((size_t)cta * 2 + slotc) * (TT * 64);
+          if (b == bA && V0 > b * NG) {
+            // publisher: band b started in an earlier CTA, whose owner pulls this partial.  Plain
+            // stores: every word is self-validating (the slot holds the sentinel until written)
+            float* part = p.ws_part + (size_t)cta * (TT * 64);
 #pragma unroll
-          for (int tk = 0; tk < TT; ++tk)
+            for (int tk = 0; tk < TT; ++tk)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) part[tk * 64 + lane + 32 * h] = v[tk][h];
-          __syncwarp();
-          unsigned int oldg = 0;
-          if (lane == 0)                                  // release our partial, acquire the others'
-            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(oldg) : "l"(p.ws_cnt + b) : "memory");
-          oldg = __shfl_sync(0xffffffffu, oldg, 0);
-          TSW(7);
-          const int cfirst = unit_owner(b * NG, p.qq, p.rr);
-          const int clast = unit_owner(min((b + 1) * NG, p.Us) - 1, p.qq, p.rr);
-          if (oldg == (unsigned int)(clast - cfirst)) {   // last CTA of the band: sum in CTA order
-            __syncwarp();
+              for (int h = 0; h < 2; ++h) __stcg(part + tk * 64 + lane + 32 * h, v[tk][h]);
+          } else {
+            // owner (we hold the band's first unit): pull the later contributors' partials, sum in
+            // CTA order, write y, re-arm their slots for the next launch
+            const int clast = unit_owner(min((b + 1) * NG, p.Us) - 1, p.qq, p.rr);
+            TSW(7);
+            for (int cb = cta + 1; cb <= clast; cb += kSumBatch) {
+              uint32_t vals[kSumBatch][TT][2];
+#pragma unroll
+              for (int j = 0; j < kSumBatch; ++j)
+#pragma unroll
+                for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+                  for (int h = 0; h < 2; ++h)
+                    vals[j][tk][h] = cb + j <= clast
+                                         ? ld_relaxed(p.ws_part + (size_t)(cb + j) * (TT * 64) + tk * 64 + lane + 32 * h)
+                                         : 0u;
+#pragma unroll
+              for (int j = 0; j < kSumBatch; ++j) {
+                if (cb + j > clast) break;
+                const unsigned int* src = reinterpret_cast<const unsigned int*>(p.ws_part) + (size_t)(cb + j) * (TT * 64);
+#pragma unroll
+                for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) {
+                    long spins = 0;
+                    while (vals[j][tk][h] == kSentinel) {       // that publisher has not written yet
+                      vals[j][tk][h] = ld_relaxed(reinterpret_cast<const float*>(src) + tk * 64 + lane + 32 * h);
+                      if (++spins > (1L << 26)) __trap();       // a publisher never arrived: fail loudly
+                    }
+                    v[tk][h] += __uint_as_float(vals[j][tk][h]);
+                  }
+              }
+            }
+            for (int c2 = cta + 1; c2 <= clast; ++c2)
+#pragma unroll
+              for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  reinterpret_cast<unsigned int*>(p.ws_part)[(size_t)c2 * (TT * 64) + tk * 64 + lane + 32 * h] = kSentinel;
 #pragma unroll
             for (int tk = 0; tk < TT; ++tk)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const int e = tk * 64 + lane + 32 * h;
-                float sum = 0.f;
-                for (int cb = cfirst; cb <= clast; cb += kSumBatch) {
-                  float vals[kSumBatch];                  // all loads of a batch in flight at once
-#pragma unroll
-                  for (int j = 0; j < kSumBatch; ++j) {
-                    const int c2 = cb + j;
-                    const int V0c = c2 * p.qq + min(c2, p.rr);
-                    vals[j] = (c2 > clast || c2 == cta)
-                                  ? 0.f
-                                  : __ldcg(p.ws_part + ((size_t)c2 * 2 + (b == V0c / NG ? 0 : 1)) * (TT * 64) + e);
-                  }
-#pragma unroll
-                  for (int j = 0; j < kSumBatch; ++j)
-                    if (cb + j <= clast) sum += cb + j == cta ? v[tk][h] : vals[j];
-                }
                 const int row = lane + 32 * h;
-                if (row < 16 * NB) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = sum;
+                if (row < 16 * NB) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
               }
-            if (lane == 0) p.ws_cnt[b] = 0u;               // reset for the next launch
           }
         }
       }
@@ -536,13 +579,12 @@ static Plan make_plan(const sbvr_weights* w) {
   return pl;
 }
 
-// workspace = [band counters: one u32 per band][partials: 2 x TT x 64 floats per CTA]
+// workspace = [partials: TT x 64 floats per CTA], initialised to kSentinel by sbvr_workspace_init
 size_t mma_workspace_bytes_(const sbvr_weights* w, int T) {
   const Plan pl = make_plan(w);
   const int TT = T < kMaxTT ? T : kMaxTT;
   const int C = pl.C_main > pl.C_tail ? pl.C_main : pl.C_tail;
-  const size_t cnt = ((size_t)pl.n_bands * 4 + 255) / 256 * 256;
-  return cnt + (size_t)C * 2 * TT * 64 * sizeof(float);
+  return (size_t)C * TT * 64 * sizeof(float);
 }
 
 template <int K, int NB, int TT, bool DEBUG>
@@ -618,12 +660,12 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
   p.P = P_debug;
   p.one = 1;
   {
+    const char* em = getenv("SBVR_EXP_MODE");
+    p.exp = em ? atoi(em) : 0;
     const char* tsp = getenv("SBVR_TS_PTR");
     p.ts = tsp ? reinterpret_cast<unsigned long long*>(strtoull(tsp, nullptr, 0)) : nullptr;
   }
-  const size_t cnt_bytes = ((size_t)pl.n_bands * 4 + 255) / 256 * 256;
-  p.ws_cnt = ws ? reinterpret_cast<unsigned int*>(ws) : nullptr;
-  p.ws_part = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + cnt_bytes) : nullptr;
+  p.ws_part = ws ? reinterpret_cast<float*>(ws) : nullptr;
   (void)ws_bytes;
   const uint32_t* xp = static_cast<const uint32_t*>(x->data);
   const bool debug = P_debug != nullptr;
@@ -639,7 +681,6 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
       const int Us = part == 0 ? pl.Us_main : pl.Us_tail;
       if (Us == 0) continue;
       p.band0 = part == 0 ? 0 : pl.n_full;
-      p.ws_cnt = ws ? reinterpret_cast<unsigned int*>(ws) + p.band0 : nullptr;
       p.Us = Us;
       p.Pw = part == 0 ? pl.C_main : pl.C_tail;
       p.qq = Us / p.Pw;

@@ -46,7 +46,7 @@ struct TcParams {
   float* Y;                 // [T][M]
   int32_t* P;               // debug partials [M][NG][K][l]
   float* ws_part;           // [C][group][TT][128] partials of each CTA's first row block when shared
-  unsigned int* ws_cnt;     // [C][group] publish flags (set by the publisher, cleared by the owner)
+  unsigned int* ws_cnt;     // [C][group] publish flags: 1 = set by the publisher, 0xFFFFFFFF = cleared (owner)
   int M, N, l, n_ratio;
   int n_full, tail_rows;    // full row blocks, rows of the tail block (0 if none)
   int Us;                   // units
@@ -455,13 +455,13 @@ __global__ void __launch_bounds__(NWG * 128 + 32, 1) gemv_tc_kernel(TcParams p) 
       do {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(p.ws_cnt + (cta + 1) * NWG + q) : "memory");
         if (++spins > (1L << 28)) __trap();     // a publisher never arrived: fail loudly, never hang
-      } while (f == 0u);
+      } while (f != 1u);
     }
     __syncthreads();
     const float* src = p.ws_part + ((size_t)(cta + 1) * NWG) * (TT * 128);
     for (int e = tid; e < nPre * TT * 128; e += blockDim.x) s_pre[e] = __ldcg(src + e);
     __syncthreads();
-    for (int q = tid; q < nPre; q += blockDim.x) p.ws_cnt[(cta + 1) * NWG + q] = 0u;   // reset for the next launch
+    for (int q = tid; q < nPre; q += blockDim.x) p.ws_cnt[(cta + 1) * NWG + q] = 0xFFFFFFFFu;   // reset for the next launch
   }
   // ---- CTA combine in (group) order; row blocks we published are finished by their owner
   const int nrb = rbZ - rbA + 1;

@@ -224,12 +224,15 @@ def test_abi_errors():
     with pytest.raises(sb.SbvrError) as e:
         sb.gemv(w, act)
     assert e.value.status == sb.ERR_SHAPE
-    act = sb.encode_vector(torch.zeros(256, dtype=torch.float16, device=DEV))
-    small = sb.Workspace(256)
+    # a matrix split over many CTAs needs cross-CTA slots: a 256-byte workspace is too small
+    pcb, s16b, b16b, rib = synthetic.random_encoded(1024, 4096, 4, 16, seed=1)
+    wb = sb.pack_canonical(pcb, s16b, b16b, rib, 16)
+    assert sb.Workspace.for_weights(wb, 1).nbytes > 256
+    actb = sb.encode_vector(torch.zeros(4096, dtype=torch.float16, device=DEV))
     with pytest.raises(sb.SbvrError) as e:
-        sb.gemv(w, act, ws=small) if sb.Workspace.for_weights(w).nbytes > 256 else (_ for _ in ()).throw(
-            sb.SbvrError(sb.ERR_WORKSPACE, "x", "y"))
+        sb.gemv(wb, actb, ws=sb.Workspace(256))
     assert e.value.status == sb.ERR_WORKSPACE
+    act = sb.encode_vector(torch.zeros(256, dtype=torch.float16, device=DEV))
     y = sb.gemv(w, act)
     torch.cuda.synchronize()
     assert not y.any()                       # zero activation -> zero output
