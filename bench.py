@@ -450,6 +450,65 @@ def standalone_per_projection(device, iters=100):
     return out
 
 
+def _time_gemv(sb, device, M, N, K, T, act_kind, algo, iters=60, seed=0):
+    """us per GEMV: CUDA graph of back-to-back launches over a ring of distinct weight copies
+    (> 2.2x L2), device time by CUDA events."""
+    pc, s16, b16, ri = synthetic.random_encoded(M, N, K, N_RATIO, seed=seed + M + N + K)
+    w0 = sb.pack_canonical(pc, s16, b16, ri, N_RATIO, device=device)
+    ring = max(2, int(2.2 * 132e6 // w0.nbytes) + 1)
+    ws_ = [w0] + [sb.SbvrWeights(M, N, K, N_RATIO, w0.data.clone(), w0.ratio_pow.clone()) for _ in range(ring - 1)]
+    wsp = [sb.Workspace.for_weights(w, T) for w in ws_]
+    x = torch.from_numpy(synthetic.activation(N, seed=6, T=T)).to(device)
+    act = sb.encode_vector(x) if act_kind == "sbvr" else sb.fp16_activation(x)
+    y = torch.empty(T, M, dtype=torch.float32, device=device)
+    stream = torch.cuda.Stream(device)
+    with torch.cuda.stream(stream):
+        for i in range(3):
+            sb.gemv_ex(ws_[i % ring], act, y=y, ws=wsp[i % ring], algo=algo)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(iters):
+                sb.gemv_ex(ws_[i % ring], act, y=y, ws=wsp[i % ring], algo=algo)
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+    us = a.elapsed_time(b) * 1e3 / iters
+    byts = sb.algorithmic_bytes(M, N, K, act=act_kind, l=L_BITS, T=T)
+    del ws_, wsp
+    torch.cuda.empty_cache()
+    return {"M": M, "N": N, "K": K, "T": T, "x": act_kind, "algo": {0: "auto", 1: "popc", 2: "tc", 3: "mma"}[algo],
+            "us": round(us, 3), "GBps": round(byts / (us * 1e-6) / 1e9, 1)}
+
+
+def sweeps(device):
+    """Configs C4/C5 and the fp16-x path: batched T, K sweep on Qwen-2.5-7B,
+    fp16-x vs SBVR-x.  Diagnostic keys; the headline stays the layer step."""
+    import paper_2509_18172_b200 as sb
+    out = {"batched": [], "k_sweep_qwen25_7b": [], "fp16x_llama3_8b": []}
+    for name, M, N in (("q_proj", 4096, 4096), ("gate_proj", 14336, 4096)):
+        for T in (1, 2, 4, 8, 16):
+            for algo in (sb.ALGO_MMA, sb.ALGO_TC):
+                r = _time_gemv(sb, device, M, N, K_BITS, T, "sbvr", algo)
+                r["proj"] = name
+                out["batched"].append(r)
+    for name, M, N in (("q_proj", 3584, 3584), ("gate_proj", 18944, 3584), ("down_proj", 3584, 18944)):
+        for K in (2, 3, 4):
+            for kind in ("sbvr", "fp16"):
+                r = _time_gemv(sb, device, M, N, K, 1, kind, sb.ALGO_AUTO)
+                r["proj"] = name
+                out["k_sweep_qwen25_7b"].append(r)
+    for name, M, N in (("q_proj", 4096, 4096), ("gate_proj", 14336, 4096), ("down_proj", 4096, 14336)):
+        for T in (1, 2, 8):
+            r = _time_gemv(sb, device, M, N, K_BITS, T, "fp16", sb.ALGO_AUTO)
+            r["proj"] = name
+            out["fp16x_llama3_8b"].append(r)
+    return out
+
+
 def encode_throughput(device):
     """Strict fp64 GPU encoder throughput on one Llama-3-8B q_proj (4096x4096, sigma 0.02): groups/s."""
     import paper_2509_18172_b200 as sb
@@ -488,6 +547,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-encode", action="store_true")
+    ap.add_argument("--no-sweeps", action="store_true")
     args = ap.parse_args()
 
     world = env_int("WORLD_SIZE", 1)
@@ -521,6 +581,11 @@ def main():
                 extra["encode"] = encode_throughput(device)
             except Exception as e:  # pragma: no cover
                 extra["encode"] = {"error": str(e)}
+        if not args.no_sweeps and world == 1:
+            try:
+                extra["sweeps"] = sweeps(device)
+            except Exception as e:  # pragma: no cover
+                extra["sweeps"] = {"error": str(e)}
         if not args.no_cpu_baseline and world == 1:
             extra["cpu"] = cpu_baseline()
     if world > 1:
@@ -602,6 +667,8 @@ def main():
             out["vs_cublas_fp16"]["speedup_gemv_only"] = round(cb["ms_per_step"] / res["span_ms_avg"], 3)
     if "encode" in extra:
         out["encode"] = extra["encode"]
+    if "sweeps" in extra:
+        out["sweeps"] = extra["sweeps"]
     if "cpu" in extra:
         out["cpu_baseline"] = extra["cpu"]
     print(json.dumps(out), flush=True)

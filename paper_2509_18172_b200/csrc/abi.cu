@@ -155,8 +155,15 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
   if (!Y) return set_error(SBVR_ERR_INVALID_ARG, "Y is NULL");
   cudaStream_t st = (cudaStream_t)stream;
   if (X->kind == SBVR_ACT_FP16) {
-    if (algo == SBVR_ALGO_TC) return set_error(SBVR_ERR_UNSUPPORTED, "tensor-memory fp16-x kernel not built");
-    return launch_gemv_fp16x(w, X, T, Y, st);
+    // fp16-x: MMA (mma.m16n8k16 f16, tokens as MMA columns) by default; POPC selects the CUDA-core
+    // reference kernel (one predicated add per set bit)
+    if (algo == SBVR_ALGO_POPC) return launch_gemv_fp16x(w, X, T, Y, st);
+    if (algo != SBVR_ALGO_AUTO && algo != SBVR_ALGO_MMA)
+      return set_error(SBVR_ERR_UNSUPPORTED, "fp16-x runs on the MMA (default) or POPC kernel, not algo %d", algo);
+    size_t need = mma_workspace_bytes(w, T);
+    if (need && (!workspace || ws_bytes < need))
+      return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    return launch_gemv_mma(w, X, T, Y, workspace, ws_bytes, nullptr, st);
   }
   if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, X, T, Y, nullptr, st);
   if (algo == SBVR_ALGO_AUTO) algo = T < kTcMinT ? SBVR_ALGO_MMA : SBVR_ALGO_TC;

@@ -52,7 +52,9 @@ constexpr unsigned int kSentinel = 0xFFFFFFFFu;   // "not yet written" (a NaN ar
 struct ImmaParams {
   const uint8_t* units;     // the weights' unit records (sbvr.h)
   const float* ratio_pow;   // [n_ratio][K]
-  const uint32_t* xplanes;  // [T][NG][l][4]
+  const uint32_t* xplanes;  // [T][NG][l][4] (SBVR-x)
+  const uint16_t* xh;       // [T][N] fp16 x (fp16-x path)
+  int ntok;                 // fp16-x: tokens in this pass (<= 8, one per MMA column)
   const float* xscales;     // [T][NG]
   float* Y;                 // [T][M]
   int32_t* P;               // debug partials [M][NG][K][l]
@@ -118,6 +120,20 @@ __device__ __forceinline__ void mma_u8(int (&d)[4], uint32_t a0, uint32_t a1, ui
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
 }
 
+__device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                        uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// fp16-x A operand: bits s and 16+s of plane word w as the fp16 pair (bit_s ? 1.0 : 0, bit_16+s ? 1.0 : 0):
+// mask (one LOP3), then one IMAD by 0x3C00 >> s turns each isolated bit into 0x3C00 (no carry between
+// halves).  Bits 11..15 are taken from w >> 5 so the multiplier stays an integer.
+__device__ __forceinline__ uint32_t f16_bits(uint32_t w, uint32_t w5, int S) {   // S is a constant after unrolling
+  if (S <= 10) return (w & (0x00010001u << S)) * (0x3C00u >> S);
+  return (w5 & (0x00010001u << (S - 5))) * (0x3C00u >> (S - 5));
+}
+
 // exact int -> float for |u| < 2^22 without the ALU pipe: (u + 0x4B400000) as float - 12582912
 __device__ __forceinline__ float i2f_fma(int u, int one) {
   int v;
@@ -173,10 +189,14 @@ __device__ __forceinline__ void issue_unit(uint8_t* slot, uint64_t* bar, const I
   bulk_g2s(slot + Gm::kPlaneBytes + Gm::kSbBytes + 16 * i0, u + (size_t)R * (16 * K + 4) + r0, nt * 16, bar);
 }
 
-template <int K, int NB, int TT, bool DEBUG>
+// F16X: the fp16-x path (north star): M_t = sum_e beta_t[e] x_e with x in fp16, on
+// mma.m16n8k16 f16 (A = plane bits as 0/1.0 pairs, B = the lane's own x values, columns = tokens);
+// TT is then the number of token columns kept (<= 8).
+template <int K, int NB, int TT, bool DEBUG, bool F16X>
 __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams p) {
   using Gm = Geom<K, NB>;
-  constexpr int PT = (NB % 2 == 0 && TT == 1) ? 2 : 1;   // tiles per compute step
+  constexpr int PT = (NB % 2 == 0 && TT == 1 && !F16X) ? 2 : 1;   // tiles per compute step
+  constexpr int NACC = F16X ? 2 : TT;                  // accumulators per tile: tokens (SBVR) or columns (F16X)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float s_rat[64];                 // r_i (fp32) for the Horner evaluation of sum_t r^t u_t
   __shared__ uint64_t s_bar[kImmaWarps][kSlots];
@@ -252,9 +272,9 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   // chunk swizzle of rows gq and gq+8 (sbvr.h; depends on the low 3 row bits only)
   const int swz_a = chunk_swizzle(K, gq), swz_b = chunk_swizzle(K, gq + 8);
 
-  float2 acc[TT][NB];
+  float2 acc[NACC][NB];
 #pragma unroll
-  for (int tk = 0; tk < TT; ++tk)
+  for (int tk = 0; tk < NACC; ++tk)
 #pragma unroll
     for (int i = 0; i < NB; ++i) acc[tk][i] = make_float2(0.f, 0.f);
 
@@ -264,24 +284,52 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   uint32_t phase = 0;
   uint32_t Xn[TT];
   float sxn[TT];
+  uint4 Xh[F16X ? 4 : 1];                              // fp16-x: x[token gq][32c .. 32c+31] of the group
+  auto load_xh = [&](int gg) {
+    if constexpr (F16X) {
+      if (gq < p.ntok) {
+        const uint4* src = reinterpret_cast<const uint4*>(p.xh + (size_t)gq * p.N + (size_t)gg * kG + 32 * c);
 #pragma unroll
-  for (int tk = 0; tk < TT; ++tk) {
-    Xn[tk] = __ldg(xlane_ptr + ((size_t)tk * NG + g) * xstride);
-    sxn[tk] = __ldg(p.xscales + (size_t)tk * NG + g);
+        for (int q = 0; q < 4; ++q) Xh[q] = __ldg(src + q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Xh[q] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+  };
+  if constexpr (F16X) {
+    load_xh(g);
+  } else {
+#pragma unroll
+    for (int tk = 0; tk < TT; ++tk) {
+      Xn[tk] = __ldg(xlane_ptr + ((size_t)tk * NG + g) * xstride);
+      sxn[tk] = __ldg(p.xscales + (size_t)tk * NG + g);
+    }
   }
 
   for (int k = 0; k < n_mine; ++k) {
     // ---- B operand for group g: activation plane gq, word c, bit-sliced and pre-scaled by 2^(7-s)
     uint32_t Bq[TT][4][2];
     float sx[TT];
+    uint32_t Bh[F16X ? 8 : 1][2];                       // fp16-x B: (x_s, x_16+s) pairs for s = 2m, 2m+1
+    if constexpr (F16X) {
+      const uint32_t xw[16] = {Xh[0].x, Xh[0].y, Xh[0].z, Xh[0].w, Xh[1].x, Xh[1].y, Xh[1].z, Xh[1].w,
+                               Xh[2].x, Xh[2].y, Xh[2].z, Xh[2].w, Xh[3].x, Xh[3].y, Xh[3].z, Xh[3].w};
 #pragma unroll
-    for (int tk = 0; tk < TT; ++tk) {
-      sx[tk] = sxn[tk];
-      const uint32_t X = Xn[tk] & xmask;
+      for (int m = 0; m < 8; ++m) {                   // xw[i] = (x_2i, x_2i+1); element e of the word at 32c+e
+        Bh[m][0] = __byte_perm(xw[m], xw[8 + m], 0x5410);   // (x_2m, x_16+2m)
+        Bh[m][1] = __byte_perm(xw[m], xw[8 + m], 0x7632);   // (x_2m+1, x_16+2m+1)
+      }
+    } else {
 #pragma unroll
-      for (int pr = 0; pr < 4; ++pr) {
-        Bq[tk][pr][0] = bslice(X, 2 * pr);
-        Bq[tk][pr][1] = bslice(X, 2 * pr + 1);
+      for (int tk = 0; tk < TT; ++tk) {
+        sx[tk] = sxn[tk];
+        const uint32_t X = Xn[tk] & xmask;
+#pragma unroll
+        for (int pr = 0; pr < 4; ++pr) {
+          Bq[tk][pr][0] = bslice(X, 2 * pr);
+          Bq[tk][pr][1] = bslice(X, 2 * pr + 1);
+        }
       }
     }
     // next unit of this warp: band/group, activation prefetch
@@ -292,10 +340,14 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     const bool has_next = k + 1 < n_mine;
     {
       const int gp = has_next ? gn : g;
+      if constexpr (F16X) {
+        load_xh(gp);
+      } else {
 #pragma unroll
-      for (int tk = 0; tk < TT; ++tk) {
-        Xn[tk] = __ldg(xlane_ptr + ((size_t)tk * NG + gp) * xstride);
-        sxn[tk] = __ldg(p.xscales + (size_t)tk * NG + gp);
+        for (int tk = 0; tk < TT; ++tk) {
+          Xn[tk] = __ldg(xlane_ptr + ((size_t)tk * NG + gp) * xstride);
+          sxn[tk] = __ldg(p.xscales + (size_t)tk * NG + gp);
+        }
       }
     }
 
@@ -326,6 +378,53 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
         sb1[j] = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq + 8) * 4);
         r2[j] = make_float2(s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq]],
                             s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq + 8]]);
+      }
+
+      if constexpr (F16X) {
+        // ---- fp16-x: M_t = sum_e beta_t[e] x_e on mma.m16n8k16 (fp32 accumulate); K chains of 8 MMAs
+        float Df[PT][K][4];
+        uint32_t w5[PT][2 * K];
+#pragma unroll
+        for (int j = 0; j < PT; ++j)
+#pragma unroll
+          for (int q = 0; q < 2 * K; ++q) w5[j][q] = w[j][q] >> 5;
+#pragma unroll
+        for (int j = 0; j < PT; ++j)
+#pragma unroll
+          for (int t = 0; t < K; ++t) Df[j][t][0] = Df[j][t][1] = Df[j][t][2] = Df[j][t][3] = 0.f;
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+#pragma unroll
+          for (int t = 0; t < K; ++t)
+#pragma unroll
+            for (int j = 0; j < PT; ++j) {
+              const uint32_t a0 = f16_bits(w[j][2 * t], w5[j][2 * t], 2 * m);
+              const uint32_t a1 = f16_bits(w[j][2 * t + 1], w5[j][2 * t + 1], 2 * m);
+              const uint32_t a2 = f16_bits(w[j][2 * t], w5[j][2 * t], 2 * m + 1);
+              const uint32_t a3 = f16_bits(w[j][2 * t + 1], w5[j][2 * t + 1], 2 * m + 1);
+              mma_f16(Df[j][t], a0, a1, a2, a3, Bh[m][0], Bh[m][1]);
+            }
+#pragma unroll
+        for (int j = 0; j < PT; ++j) {
+          const int i = ib + j;
+          const float2 s2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0[j] & 0xffffu))),
+                                        __half2float(__ushort_as_half((unsigned short)(sb1[j] & 0xffffu))));
+          const float2 b2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0[j] >> 16))),
+                                        __half2float(__ushort_as_half((unsigned short)(sb1[j] >> 16))));
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {                 // MMA column 2c+h = token 2c+h; rows (gq, gq+8)
+            float2 Ph = make_float2(Df[j][K - 1][h], Df[j][K - 1][2 + h]);
+            float2 U = Ph;
+#pragma unroll
+            for (int t = K - 2; t >= 0; --t) {
+              const float2 f = make_float2(Df[j][t][h], Df[j][t][2 + h]);
+              Ph = __ffma2_rn(Ph, r2[j], f);
+              U = __fadd2_rn(U, f);
+            }
+            acc[h][i] = __fadd2_rn(acc[h][i], __ffma2_rn(s2, Ph, __fmul2_rn(b2, U)));
+          }
+        }
+        continue;
       }
 
       // ---- AND + popcount on the tensor pipe: PT x K independent chains (tile, plane) of 4 MMAs
@@ -415,6 +514,19 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
       const int wf = __ffs(holders) - 1, wl = 31 - __clz(holders);
       const bool shared = V0 > b * NG || V1 < min((b + 1) * NG, p.Us);    // other CTAs hold units of b
       float* sp = s_part + ((size_t)wib * 2 + (b == s_fb[wib] ? 0 : 1)) * (TT * 64);
+      if constexpr (F16X) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            const int col = 2 * c + h;                   // token of this MMA column
+            if (col < TT) {
+              sp[col * 64 + 16 * i + gq] = acc[h][i].x;
+              sp[col * 64 + 16 * i + gq + 8] = acc[h][i].y;
+            }
+            acc[h][i] = make_float2(0.f, 0.f);
+          }
+      } else {
 #pragma unroll
       for (int tk = 0; tk < TT; ++tk)
 #pragma unroll
@@ -430,6 +542,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
           }
           acc[tk][i] = make_float2(0.f, 0.f);
         }
+      }
       bool last = true;
       if (wf != wl) {
         __syncwarp();
@@ -582,17 +695,17 @@ static Plan make_plan(const sbvr_weights* w) {
 // workspace = [partials: TT x 64 floats per CTA], initialised to kSentinel by sbvr_workspace_init
 size_t mma_workspace_bytes_(const sbvr_weights* w, int T) {
   const Plan pl = make_plan(w);
-  const int TT = T < kMaxTT ? T : kMaxTT;
+  const int TT = T < 8 ? T : 8;                       // fp16-x passes keep up to 8 token columns
   const int C = pl.C_main > pl.C_tail ? pl.C_main : pl.C_tail;
   return (size_t)C * TT * 64 * sizeof(float);
 }
 
-template <int K, int NB, int TT, bool DEBUG>
+template <int K, int NB, int TT, bool DEBUG, bool F16X>
 static cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
   const int smem = kImmaWarps * Geom<K, NB>::kWarpBytes + kImmaWarps * 2 * TT * 64 * 4;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG>,
+    cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG, F16X>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -607,39 +720,47 @@ static cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
   attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr_pdl;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG>, p);
+  return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG, F16X>, p);
 }
 
 template <int K, int NB>
-static cudaError_t launch_nb(const ImmaParams& p, int TT, bool debug, cudaStream_t st) {
-  if (debug) return launch_one<K, NB, 1, true>(p, st);
+static cudaError_t launch_nb(const ImmaParams& p, int TT, bool debug, bool f16x, cudaStream_t st) {
+  if (f16x) {
+    switch (TT) {
+      case 1: return launch_one<K, NB, 1, false, true>(p, st);
+      case 2: return launch_one<K, NB, 2, false, true>(p, st);
+      case 4: return launch_one<K, NB, 4, false, true>(p, st);
+      default: return launch_one<K, NB, 8, false, true>(p, st);
+    }
+  }
+  if (debug) return launch_one<K, NB, 1, true, false>(p, st);
   switch (TT) {
-    case 1: return launch_one<K, NB, 1, false>(p, st);
-    case 2: return launch_one<K, NB, 2, false>(p, st);
-    default: return launch_one<K, NB, 4, false>(p, st);
+    case 1: return launch_one<K, NB, 1, false, false>(p, st);
+    case 2: return launch_one<K, NB, 2, false, false>(p, st);
+    default: return launch_one<K, NB, 4, false, false>(p, st);
   }
 }
 
 template <int K>
-static cudaError_t launch_k(const ImmaParams& p, int NB, int TT, bool debug, cudaStream_t st) {
+static cudaError_t launch_k(const ImmaParams& p, int NB, int TT, bool debug, bool f16x, cudaStream_t st) {
   switch (NB) {
-    case 4: return launch_nb<K, 4>(p, TT, debug, st);
-    case 3: return launch_nb<K, 3>(p, TT, debug, st);
-    case 2: return launch_nb<K, 2>(p, TT, debug, st);
-    default: return launch_nb<K, 1>(p, TT, debug, st);
+    case 4: return launch_nb<K, 4>(p, TT, debug, f16x, st);
+    case 3: return launch_nb<K, 3>(p, TT, debug, f16x, st);
+    case 2: return launch_nb<K, 2>(p, TT, debug, f16x, st);
+    default: return launch_nb<K, 1>(p, TT, debug, f16x, st);
   }
 }
 
-static cudaError_t launch_any(int K, const ImmaParams& p, int NB, int TT, bool debug, cudaStream_t st) {
+static cudaError_t launch_any(int K, const ImmaParams& p, int NB, int TT, bool debug, bool f16x, cudaStream_t st) {
   switch (K) {
-    case 1: return launch_k<1>(p, NB, TT, debug, st);
-    case 2: return launch_k<2>(p, NB, TT, debug, st);
-    case 3: return launch_k<3>(p, NB, TT, debug, st);
-    case 4: return launch_k<4>(p, NB, TT, debug, st);
-    case 5: return launch_k<5>(p, NB, TT, debug, st);
-    case 6: return launch_k<6>(p, NB, TT, debug, st);
-    case 7: return launch_k<7>(p, NB, TT, debug, st);
-    default: return launch_k<8>(p, NB, TT, debug, st);
+    case 1: return launch_k<1>(p, NB, TT, debug, f16x, st);
+    case 2: return launch_k<2>(p, NB, TT, debug, f16x, st);
+    case 3: return launch_k<3>(p, NB, TT, debug, f16x, st);
+    case 4: return launch_k<4>(p, NB, TT, debug, f16x, st);
+    case 5: return launch_k<5>(p, NB, TT, debug, f16x, st);
+    case 6: return launch_k<6>(p, NB, TT, debug, f16x, st);
+    case 7: return launch_k<7>(p, NB, TT, debug, f16x, st);
+    default: return launch_k<8>(p, NB, TT, debug, f16x, st);
   }
 }
 
@@ -667,14 +788,21 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
   }
   p.ws_part = ws ? reinterpret_cast<float*>(ws) : nullptr;
   (void)ws_bytes;
-  const uint32_t* xp = static_cast<const uint32_t*>(x->data);
+  const bool f16x = x->kind == SBVR_ACT_FP16;
+  const uint32_t* xp = f16x ? nullptr : static_cast<const uint32_t*>(x->data);
+  const uint16_t* xh = f16x ? static_cast<const uint16_t*>(x->data) : nullptr;
   const bool debug = P_debug != nullptr;
   int done = 0;
   while (done < T) {
     const int rem = T - done;
-    const int TT = debug ? 1 : (rem >= 4 ? 4 : (rem >= 2 ? 2 : 1));
-    p.xplanes = xp + (size_t)done * pl.NG * x->l * 4;
-    p.xscales = x->scales + (size_t)done * pl.NG;
+    int TT;
+    if (f16x) TT = rem >= 8 ? 8 : (rem > 4 ? 8 : (rem > 2 ? 4 : rem));   // token columns of mma.m16n8k16
+    else TT = debug ? 1 : (rem >= 4 ? 4 : (rem >= 2 ? 2 : 1));
+    const int ntok = rem < TT ? rem : TT;
+    p.ntok = ntok;
+    p.xplanes = f16x ? nullptr : xp + (size_t)done * pl.NG * x->l * 4;
+    p.xscales = f16x ? nullptr : x->scales + (size_t)done * pl.NG;
+    p.xh = f16x ? xh + (size_t)done * w->N : nullptr;
     p.Y = Y ? Y + (size_t)done * w->M : nullptr;
     for (int part = 0; part < 2; ++part) {
       const int NB = part == 0 ? 4 : pl.tail_nb;
@@ -685,13 +813,13 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
       p.Pw = part == 0 ? pl.C_main : pl.C_tail;
       p.qq = Us / p.Pw;
       p.rr = Us % p.Pw;
-      cudaError_t e = launch_any(w->K, p, NB, TT, debug, st);
+      cudaError_t e = launch_any(w->K, p, NB, TT, debug, f16x, st);
       if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "gemv_mma setup: %s", cudaGetErrorString(e));
       sbvr_status s = check_launch("gemv_mma_kernel");
       if (s != SBVR_OK) return s;
     }
     if (debug) break;
-    done += TT;
+    done += ntok;
   }
   return SBVR_OK;
 }

@@ -159,12 +159,13 @@ def test_gemv_on_gpu_encoded_weights_matches_oracle_end_to_end():
 
 
 # ------------------------------------------------------------------ a6: fp16-x GEMV
-@pytest.mark.parametrize("M,N,K", [(16, 128, 4), (80, 384, 3), (256, 1024, 2)])
-def test_gemv_fp16_x(M, N, K):
+@pytest.mark.parametrize("M,N,K", [(16, 128, 4), (80, 384, 3), (256, 1024, 2), (336, 640, 4), (1024, 512, 4)])
+@pytest.mark.parametrize("algo", [sb.ALGO_AUTO, sb.ALGO_POPC])
+def test_gemv_fp16_x(M, N, K, algo):
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=M + N)
     w = sb.pack_canonical(pc, s16, b16, ri, 16)
     x = synthetic.activation(N, seed=3)
-    y = sb.gemv(w, sb.fp16_activation(torch.from_numpy(x[0]).to(DEV)))
+    y = sb.gemv_ex(w, sb.fp16_activation(torch.from_numpy(x[0]).to(DEV)), algo=algo)[0]
     torch.cuda.synchronize()
     enc = _oracle_encoded(pc, s16, b16, ri, K, 16)
     assert_close(y.cpu().numpy(), oracle.gemv_rows(enc, oracle.x_dec_fp16(x[0])))
@@ -214,6 +215,10 @@ def test_gemv_full_size_sampled_rows(name, M, N, algo):
     P = sb.debug_partials(w, act, algo=algo)
     Pref, _ = oracle.partials_rows(enc, z, xp, rows=rows[:16])
     assert np.array_equal(P.cpu().numpy()[rows[:16]], Pref)
+    if algo == sb.ALGO_MMA:                       # fp16-x path on the same weights, same launch config
+        yf = sb.gemv_ex(w, sb.fp16_activation(torch.from_numpy(x[0]).to(DEV)), ws=ws)[0]
+        torch.cuda.synchronize()
+        assert_close(yf.cpu().numpy()[rows], oracle.gemv_rows(enc, oracle.x_dec_fp16(x[0]), rows))
 
 
 # ------------------------------------------------------------------ error behaviour

@@ -17,6 +17,7 @@ ap.add_argument("--K", type=int, default=4)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--algo", default="3", help="comma list: 1 popc, 2 tc, 3 mma")
 ap.add_argument("--T", default="1", help="comma list of batch sizes")
+ap.add_argument("--x", default="sbvr", choices=["sbvr", "fp16"], help="activation path")
 a = ap.parse_args()
 shapes = {n: (M, N) for n, M, N in synthetic.LLAMA3_8B_LAYER + [("70b_down", 8192, 28672), ("70b_gate", 28672, 8192)]}
 for name in a.shapes.split(","):
@@ -28,7 +29,7 @@ for name in a.shapes.split(","):
     ws_list = [w0] + [sb.SbvrWeights(M, N, a.K, 16, w0.data.clone(), w0.ratio_pow.clone()) for _ in range(ring - 1)]
     for T in [int(t) for t in a.T.split(",")]:
         x = torch.from_numpy(synthetic.activation(N, seed=6, T=T)).cuda()
-        act = sb.encode_vector(x)
+        act = sb.encode_vector(x) if a.x == "sbvr" else sb.fp16_activation(x)
         wss = [sb.Workspace.for_weights(w, T) for w in ws_list]
         y = torch.empty(T, M, dtype=torch.float32, device="cuda")
         for algo in [int(v) for v in a.algo.split(",")]:
@@ -49,6 +50,6 @@ for name in a.shapes.split(","):
                 e1.record(st)
                 torch.cuda.synchronize()
             us = e0.elapsed_time(e1) * 1e3 / a.iters
-            byts = sb.algorithmic_bytes(M, N, a.K)
-            print(json.dumps({"shape": name, "M": M, "N": N, "K": a.K, "algo": algo, "T": T, "ring": ring,
+            byts = sb.algorithmic_bytes(M, N, a.K, act=a.x, T=T)
+            print(json.dumps({"shape": name, "M": M, "N": N, "K": a.K, "algo": algo, "T": T, "x": a.x, "ring": ring,
                               "us": round(us, 3), "GBps": round(byts / (us * 1e-6) / 1e9, 1)}), flush=True)
