@@ -229,6 +229,13 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   };
   uint8_t* ring = smem + wib * Gm::kWarpBytes;
   uint64_t* bars = s_bar[wib];
+  int ib_band = uf / NG, ib_g = uf - (uf / NG) * NG;   // lane 0: (band, group) of the next unit to fetch
+  auto issue_next = [&](uint8_t* slot_ptr, uint64_t* bar, int kk) {
+    int i0, i1;
+    tiles_of(kk, i0, i1);
+    issue_unit<K, NB>(slot_ptr, bar, p, p.band0 + ib_band, ib_g, i0, i1);
+    if (++ib_g == NG) { ib_g = 0; ++ib_band; }
+  };
   if (n_mine > 0 && lane == 0) {
     // weights are immutable: their TMA starts before we wait for the previous kernel
 #pragma unroll
@@ -236,11 +243,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
     for (int s2 = 0; s2 < kSlots; ++s2)
-      if (s2 < n_mine && !(p.exp & 2)) {
-        int i0, i1;
-        tiles_of(s2, i0, i1);
-        issue_unit<K, NB>(ring + s2 * Gm::kSlotBytes, bars + s2, p, p.band0 + (uf + s2) / NG, (uf + s2) % NG, i0, i1);
-      }
+      if (s2 < n_mine && !(p.exp & 2)) issue_next(ring + s2 * Gm::kSlotBytes, bars + s2, s2);
   }
   for (int i = threadIdx.x; i < p.n_ratio; i += blockDim.x) s_rat[i] = K >= 2 ? p.ratio_pow[i * K + 1] : 0.f;
   for (int i = threadIdx.x; i < 2 * kImmaWarps; i += blockDim.x) s_cnt[i] = 0u;
@@ -261,8 +264,8 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   const int al1 = j1 < p.l - 1 ? (1 << j1) : (j1 == p.l - 1 ? -(1 << j1) : 0);
   const int kappa = al0 != 0 ? al1 / al0 : 0;
   const float lane_scale = (float)al0 * (1.0f / 128.0f);
-  // column 2c of every accumulator starts at 1.5*2^23 (as float bits): u = D0 + kappa*D1 is then
-  // the float 1.5*2^23 + 128 (P_2c + kappa P_2c+1), exact, with no int->float conversion
+  // u = D0 + kappa*D1 (exact int, |u| < 2^22) is converted on the FMA pipe: (u + 0x4B400000) read as
+  // a float is 1.5*2^23 + u exactly, minus 1.5*2^23 (FADD2 for the two rows of the lane)
   const int magic = 0x4B400000;
   const float2 cmagic = make_float2(12582912.0f, 12582912.0f);
   // lanes whose activation plane gq >= l contribute 0: their B words are masked at use time
@@ -441,8 +444,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 #pragma unroll
             for (int tk = 0; tk < TT; ++tk) {
               if (pr == 0)
-                mma_u8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], DEBUG ? 0 : magic, 0,
-                       DEBUG ? 0 : magic, 0);
+                mma_u8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], 0, 0, 0, 0);
               else
                 mma_u8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], D[j][tk][t][0], D[j][tk][t][1],
                        D[j][tk][t][2], D[j][tk][t][3]);
@@ -471,14 +473,14 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 #pragma unroll
           for (int tk = 0; tk < TT; ++tk) {
             // f_t = 128 (P_2c + kappa P_2c+1) for rows (gq, gq+8), exact; Horner over t in fp32x2
-            float2 Ph = __fadd2_rn(make_float2(__int_as_float(imad(D[j][tk][K - 1][1], kappa, D[j][tk][K - 1][0])),
-                                               __int_as_float(imad(D[j][tk][K - 1][3], kappa, D[j][tk][K - 1][2]))),
+            float2 Ph = __fadd2_rn(make_float2(__int_as_float(imad(imad(D[j][tk][K - 1][1], kappa, D[j][tk][K - 1][0]), p.one, magic)),
+                                               __int_as_float(imad(imad(D[j][tk][K - 1][3], kappa, D[j][tk][K - 1][2]), p.one, magic))),
                                    make_float2(-cmagic.x, -cmagic.y));
             float2 U = Ph;
 #pragma unroll
             for (int t = K - 2; t >= 0; --t) {
-              const float2 f = __fadd2_rn(make_float2(__int_as_float(imad(D[j][tk][t][1], kappa, D[j][tk][t][0])),
-                                                      __int_as_float(imad(D[j][tk][t][3], kappa, D[j][tk][t][2]))),
+              const float2 f = __fadd2_rn(make_float2(__int_as_float(imad(imad(D[j][tk][t][1], kappa, D[j][tk][t][0]), p.one, magic)),
+                                                      __int_as_float(imad(imad(D[j][tk][t][3], kappa, D[j][tk][t][2]), p.one, magic))),
                                           make_float2(-cmagic.x, -cmagic.y));
               Ph = __ffma2_rn(Ph, r2[j], f);
               U = __fadd2_rn(U, f);
@@ -494,10 +496,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     __syncwarp();
     if (lane == 0 && k + kSlots < n_mine && !(p.exp & 2)) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int u2 = uf + k + kSlots;
-      int i0, i1;
-      tiles_of(k + kSlots, i0, i1);
-      issue_unit<K, NB>(sl, bars + slot, p, p.band0 + u2 / NG, u2 % NG, i0, i1);
+      issue_next(sl, bars + slot, k + kSlots);
     }
     if (++slot == kSlots) { slot = 0; phase ^= 1u; }
 
