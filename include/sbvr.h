@@ -83,8 +83,11 @@ typedef enum { SBVR_ACT_FP16 = 0, SBVR_ACT_SBVR = 1 } sbvr_act_kind;
  *          tensor memory, B = d_j bit-sliced x 2^(7-s) in shared memory, tcgen05.mma kind::i8
  *          M=128 N=8T K=32, which counts popc(beta_t & d_j) for 128 rows x 8 planes x T tokens.
  *  MMA   : the same bit-sliced popcount with warp-level mma.sync.m16n8k32.u8 (16 rows x 8 planes
- *          per instruction), the faster issue rate at batch 1.                                  */
-typedef enum { SBVR_ALGO_AUTO = 0, SBVR_ALGO_POPC = 1, SBVR_ALGO_TC = 2, SBVR_ALGO_MMA = 3 } sbvr_algo;
+ *          per instruction), the faster issue rate at batch 1.
+ *  PIPE  : the MMA formulation in a persistent warp-specialised kernel (producer warp + CTA-wide TMA
+ *          ring, dynamically ticketed work items, deterministic split-K combine); batch 1, SBVR-x.
+ *          Explicit only: measured slower than MMA on the Llama-3-8B step.          */
+typedef enum { SBVR_ALGO_AUTO = 0, SBVR_ALGO_POPC = 1, SBVR_ALGO_TC = 2, SBVR_ALGO_MMA = 3, SBVR_ALGO_PIPE = 4 } sbvr_algo;
 
 /* Offline encoder knobs (SURVEY §8c.3 readings A1, A4). */
 typedef struct {

@@ -25,7 +25,7 @@ _lib = None
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_ALIGNMENT, ERR_CUDA, ERR_WORKSPACE = range(7)
 F32, F16, BF16 = 0, 1, 2
 ACT_FP16, ACT_SBVR = 0, 1
-ALGO_AUTO, ALGO_POPC, ALGO_TC, ALGO_MMA = 0, 1, 2, 3
+ALGO_AUTO, ALGO_POPC, ALGO_TC, ALGO_MMA, ALGO_PIPE = 0, 1, 2, 3, 4
 G = 128
 
 

@@ -2,6 +2,7 @@
 // size queries, host-side layout transforms and dispatch to the kernels.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "sbvr_internal.cuh"
@@ -133,8 +134,9 @@ sbvr_status sbvr_gemv_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* 
   if (T < 1 || T > kMaxT) return set_error(SBVR_ERR_SHAPE, "T=%d outside 1..16", T);
   if (w->M <= 0 || w->N <= 0 || w->M % kTileRows || w->N % kG)
     return set_error(SBVR_ERR_SHAPE, "bad M/N %d/%d", w->M, w->N);
-  const size_t a = tc_workspace_bytes(w, T), b = mma_workspace_bytes(w, T);
+  const size_t a = tc_workspace_bytes(w, T), b = mma_workspace_bytes(w, T), c = pipe_workspace_bytes(w);
   *bytes = a > b ? a : b;
+  if (c > *bytes) *bytes = c;
   return SBVR_OK;
 }
 
@@ -165,8 +167,21 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
       return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
     return launch_gemv_mma(w, X, T, Y, workspace, ws_bytes, nullptr, st);
   }
+  if (algo == SBVR_ALGO_AUTO) {
+    // diagnostics only (A/B timing in tools/): SBVR_FORCE_ALGO=<sbvr_algo> overrides AUTO for SBVR-x
+    static const int forced = getenv("SBVR_FORCE_ALGO") ? atoi(getenv("SBVR_FORCE_ALGO")) : 0;
+    if (forced > 0 && forced <= SBVR_ALGO_PIPE && !(forced == SBVR_ALGO_PIPE && T != 1)) algo = forced;
+  }
   if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, X, T, Y, nullptr, st);
-  if (algo == SBVR_ALGO_AUTO) algo = T < kTcMinT ? SBVR_ALGO_MMA : SBVR_ALGO_TC;
+  if (algo == SBVR_ALGO_AUTO)
+    algo = T < kTcMinT ? SBVR_ALGO_MMA : SBVR_ALGO_TC;   // PIPE is explicit-only (slower, profiles/r01_pipe_ab.txt)
+  if (algo == SBVR_ALGO_PIPE) {
+    if (T != 1) return set_error(SBVR_ERR_UNSUPPORTED, "PIPE runs batch 1 (T=%d)", T);
+    size_t need = pipe_workspace_bytes(w);
+    if (!workspace || ws_bytes < need)
+      return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    return launch_gemv_pipe(w, X, Y, workspace, nullptr, st);
+  }
   if (algo != SBVR_ALGO_TC && algo != SBVR_ALGO_MMA) return set_error(SBVR_ERR_INVALID_ARG, "bad algo %d", algo);
   size_t need = algo == SBVR_ALGO_TC ? tc_workspace_bytes(w, T) : mma_workspace_bytes(w, T);
   if (need && (!workspace || ws_bytes < need))
@@ -196,6 +211,7 @@ sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_
   if (algo == SBVR_ALGO_TC) return launch_gemv_tc(w, x, 1, nullptr, nullptr, 0, P, (cudaStream_t)stream);
   if (algo == SBVR_ALGO_MMA || algo == SBVR_ALGO_AUTO)
     return launch_gemv_mma(w, x, 1, nullptr, nullptr, 0, P, (cudaStream_t)stream);
+  if (algo == SBVR_ALGO_PIPE) return launch_gemv_pipe(w, x, nullptr, nullptr, P, (cudaStream_t)stream);
   return set_error(SBVR_ERR_INVALID_ARG, "bad algo %d", algo);
 }
 

@@ -593,30 +593,31 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
             TSW(7);
             for (int cb = cta + 1; cb <= clast; cb += kSumBatch) {
               uint32_t vals[kSumBatch][TT][2];
+              // reload the whole batch until no word is the sentinel (a publisher has not written yet):
+              // one L2 round trip per poll, not one per stale word
+              for (long spins = 0;; ++spins) {
+                bool miss = false;
 #pragma unroll
-              for (int j = 0; j < kSumBatch; ++j)
+                for (int j = 0; j < kSumBatch; ++j)
 #pragma unroll
-                for (int tk = 0; tk < TT; ++tk)
+                  for (int tk = 0; tk < TT; ++tk)
 #pragma unroll
-                  for (int h = 0; h < 2; ++h)
-                    vals[j][tk][h] = cb + j <= clast
-                                         ? ld_relaxed(p.ws_part + (size_t)(cb + j) * (TT * 64) + tk * 64 + lane + 32 * h)
-                                         : 0u;
+                    for (int h = 0; h < 2; ++h) {
+                      vals[j][tk][h] = cb + j <= clast
+                                           ? ld_relaxed(p.ws_part + (size_t)(cb + j) * (TT * 64) + tk * 64 + lane + 32 * h)
+                                           : 0u;
+                      miss |= vals[j][tk][h] == kSentinel;
+                    }
+                if (!__any_sync(0xffffffffu, miss)) break;
+                if (spins > (1L << 24)) __trap();               // a publisher never arrived: fail loudly
+              }
 #pragma unroll
               for (int j = 0; j < kSumBatch; ++j) {
                 if (cb + j > clast) break;
-                const unsigned int* src = reinterpret_cast<const unsigned int*>(p.ws_part) + (size_t)(cb + j) * (TT * 64);
 #pragma unroll
                 for (int tk = 0; tk < TT; ++tk)
 #pragma unroll
-                  for (int h = 0; h < 2; ++h) {
-                    long spins = 0;
-                    while (vals[j][tk][h] == kSentinel) {       // that publisher has not written yet
-                      vals[j][tk][h] = ld_relaxed(reinterpret_cast<const float*>(src) + tk * 64 + lane + 32 * h);
-                      if (++spins > (1L << 26)) __trap();       // a publisher never arrived: fail loudly
-                    }
-                    v[tk][h] += __uint_as_float(vals[j][tk][h]);
-                  }
+                  for (int h = 0; h < 2; ++h) v[tk][h] += __uint_as_float(vals[j][tk][h]);
               }
             }
             for (int c2 = cta + 1; c2 <= clast; ++c2)

@@ -80,5 +80,9 @@ size_t tc_workspace_bytes(const sbvr_weights* w, int T);
 sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
                             int32_t* P_debug, cudaStream_t st);
 size_t mma_workspace_bytes(const sbvr_weights* w, int T);
+sbvr_status launch_gemv_pipe(const sbvr_weights* w, const sbvr_act* x, float* y, void* ws, int32_t* P_debug,
+                             cudaStream_t st);
+size_t pipe_workspace_bytes(const sbvr_weights* w);
+bool pipe_supported(const sbvr_weights* w, const sbvr_act* x);
 
 }  // namespace sbvr

@@ -106,7 +106,7 @@ SHAPES = [(16, 128), (64, 256), (80, 384), (208, 1024), (1024, 512), (336, 640),
 
 @pytest.mark.parametrize("M,N", SHAPES)
 @pytest.mark.parametrize("K", [2, 3, 4])
-@pytest.mark.parametrize("algo", [sb.ALGO_MMA, sb.ALGO_TC, sb.ALGO_POPC])
+@pytest.mark.parametrize("algo", [sb.ALGO_PIPE, sb.ALGO_MMA, sb.ALGO_TC, sb.ALGO_POPC])
 def test_gemv_sbvr_x(M, N, K, algo):
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=M * 7 + N + K)
     w = sb.pack_canonical(pc, s16, b16, ri, 16)
@@ -124,7 +124,7 @@ def test_gemv_sbvr_x(M, N, K, algo):
 
 
 @pytest.mark.parametrize("l", [8, 6, 5, 4, 2])
-@pytest.mark.parametrize("algo", [sb.ALGO_MMA, sb.ALGO_TC])
+@pytest.mark.parametrize("algo", [sb.ALGO_PIPE, sb.ALGO_MMA, sb.ALGO_TC])
 def test_gemv_sbvr_x_activation_bits(l, algo):
     M, N, K = 48, 256, 4
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=l)
@@ -194,7 +194,7 @@ def test_gemv_batched(T, algo):
 @pytest.mark.parametrize("name,M,N", synthetic.LLAMA3_8B_LAYER + [("70b_down", 8192, 28672),
                                                                    ("gate_up_fused", 28672, 4096),
                                                                    ("tall_narrow", 16384, 256)])
-@pytest.mark.parametrize("algo", [sb.ALGO_MMA, sb.ALGO_TC])
+@pytest.mark.parametrize("algo", [sb.ALGO_PIPE, sb.ALGO_MMA, sb.ALGO_TC])
 def test_gemv_full_size_sampled_rows(name, M, N, algo):
     K = 4
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=M ^ N)
@@ -219,6 +219,26 @@ def test_gemv_full_size_sampled_rows(name, M, N, algo):
         yf = sb.gemv_ex(w, sb.fp16_activation(torch.from_numpy(x[0]).to(DEV)), ws=ws)[0]
         torch.cuda.synchronize()
         assert_close(yf.cpu().numpy()[rows], oracle.gemv_rows(enc, oracle.x_dec_fp16(x[0]), rows))
+
+
+def test_pipe_ticket_counter_rearmed_across_launches():
+    """The persistent kernel's dynamic work counter and partial slots must be back at rest after
+    every launch: many back-to-back launches on one workspace (different shapes), every result
+    checked against the oracle and against a re-run."""
+    ws = sb.Workspace(64 << 20)
+    for i, (M, N) in enumerate([(4096, 4096), (1024, 4096), (16, 128), (6144, 4096), (4096, 14336), (4096, 4096)]):
+        pc, s16, b16, ri = synthetic.random_encoded(M, N, 4, 16, seed=100 + i)
+        w = sb.pack_canonical(pc, s16, b16, ri, 16)
+        x = synthetic.activation(N, seed=200 + i)
+        act = sb.encode_vector(torch.from_numpy(x).to(DEV))
+        ys = [sb.gemv_ex(w, act, ws=ws, algo=sb.ALGO_PIPE)[0] for _ in range(3)]
+        torch.cuda.synchronize()
+        assert all(torch.equal(ys[0], y) for y in ys[1:])
+        rows = np.unique(np.concatenate([np.random.default_rng(i).choice(M, min(M, 64), replace=False), [0, M - 1]]))
+        z, xp, sc = oracle.encode_vector(x[0], 128, 8)
+        enc = _oracle_encoded(pc, s16, b16, ri, 4, 16)
+        assert_close(ys[0].cpu().numpy()[rows], oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc), rows))
+    assert torch.all(ws.buf.view(torch.int32) == -1)   # every slot and the counter re-armed
 
 
 # ------------------------------------------------------------------ error behaviour
