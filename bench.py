@@ -509,6 +509,44 @@ def sweeps(device):
     return out
 
 
+def hadamard_throughput(device):
+    """f4: randomized 128-block Hadamard rotation -- GB/s (read + write) rotating the fp32 Llama-3-8B
+    down_proj weight (offline, before encoding) and the step's 4 fp16 activations (online), plus its
+    effect on the encoder's mean group MSE for Student-t(3) weights (rotated-domain MSE = original-domain
+    MSE: the rotation is orthogonal)."""
+    import paper_2509_18172_b200 as sb
+    out = {}
+    for name, rows, N, dt in (("down_proj_weight_fp32", 4096, 14336, torch.float32),
+                              ("step_activations_fp16", 4, 14336, torch.float16)):
+        X = torch.randn(rows, N, device=device).to(dt)
+        sg = torch.from_numpy(synthetic.hadamard_signs(N, seed=5)).to(device)
+        Y = torch.empty_like(X)
+        it = 20 if rows > 4 else 200
+        st = torch.cuda.Stream(device)
+        with torch.cuda.stream(st):
+            sb.hadamard_rows(X, sg, 128, out=Y)
+            g = torch.cuda.CUDAGraph()                   # launch-bound at the activation size: graph it
+            with torch.cuda.graph(g, stream=st):
+                for _ in range(it):
+                    sb.hadamard_rows(X, sg, 128, out=Y)
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            g.replay()
+            b.record(st)
+        torch.cuda.synchronize()
+        us = a.elapsed_time(b) * 1e3 / it
+        by = 2 * X.numel() * X.element_size()
+        out[name] = {"rows": rows, "N": N, "block": 128, "us": round(us, 3), "GBps": round(by / us / 1e3, 1)}
+    W = torch.from_numpy(synthetic.student_t_weight(512, 4096, seed=77)).to(device)
+    sg = torch.from_numpy(synthetic.hadamard_signs(4096, seed=78)).to(device)
+    _, m0 = sb.encode_weights(W, K=K_BITS, return_mse=True)
+    _, m1 = sb.encode_weights(sb.hadamard_rows(W, sg, 128), K=K_BITS, return_mse=True)
+    out["student_t3_512x4096_mean_group_mse"] = {"plain": m0.mean().item(), "rotated_b128": m1.mean().item()}
+    return out
+
+
 def encode_throughput(device):
     """Strict fp64 GPU encoder throughput on one Llama-3-8B q_proj (4096x4096, sigma 0.02): groups/s."""
     import paper_2509_18172_b200 as sb
@@ -579,6 +617,7 @@ def main():
         if not args.no_encode:
             try:
                 extra["encode"] = encode_throughput(device)
+                extra["hadamard"] = hadamard_throughput(device)
             except Exception as e:  # pragma: no cover
                 extra["encode"] = {"error": str(e)}
         if not args.no_sweeps and world == 1:
@@ -667,6 +706,8 @@ def main():
             out["vs_cublas_fp16"]["speedup_gemv_only"] = round(cb["ms_per_step"] / res["span_ms_avg"], 3)
     if "encode" in extra:
         out["encode"] = extra["encode"]
+    if "hadamard" in extra:
+        out["hadamard"] = extra["hadamard"]
     if "sweeps" in extra:
         out["sweeps"] = extra["sweeps"]
     if "cpu" in extra:

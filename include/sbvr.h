@@ -164,6 +164,17 @@ sbvr_status sbvr_gemv_batched(const sbvr_weights* w, const sbvr_act* X, int32_t 
 sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
                          size_t ws_bytes, int32_t algo, void* stream);
 
+/* sbvr_hadamard_rows -- randomized Hadamard rotation, P:255 (Section 4.5): "rotate the weights with a
+ * randomized Hadamard transform to Gaussianize them and suppress outliers" before encoding (and the
+ * activations with the same orthogonal Q, since W x = (W Q^T)(Q x)).  Reading A21: block-diagonal along
+ * N; every block of `block` consecutive columns of every row becomes
+ *     Y[r, blk*b + i] = sum_k (-1)^popcount(i & k) * signs[blk*b + k] * X[r, blk*b + k] / sqrt(b).
+ * X, Y: device, row-major [rows][N], dtype SBVR_F32 or SBVR_F16 (fp32 arithmetic); Y == X allowed
+ * (in place).  signs: device int8 [N], each +1 or -1 (the random diagonal D, caller-drawn).  block: a
+ * power of two in 32..1024 with N % block == 0 (SBVR_ERR_UNSUPPORTED / SBVR_ERR_SHAPE otherwise).
+ * Buffers 16-byte aligned. */
+sbvr_status sbvr_hadamard_rows(const void* X, void* Y, int32_t dtype, int32_t rows, int32_t N, int32_t block,
+                               const int8_t* signs, void* stream);
 /* Test-only: the integer popcount partials P[m][g][t][j] = popc(beta_t & d_j) over the group,
  * int32 [M][N/G][K][l] row-major (device), computed by the kernel `algo` (POPC, TC or MMA) from an
  * SBVR-x activation (T = 1). */

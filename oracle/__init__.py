@@ -83,6 +83,7 @@ def lib():
         L.oracle_gemv_rows.argtypes = [P, P, P, P, i32, i32, i32, i32, i32, P, P, i32, P]
         L.oracle_partials_rows.argtypes = [P, P, P, i32, i32, i32, i32, P, i32, P, P]
         L.oracle_max_threads.restype = i32
+        L.oracle_hadamard_rows.argtypes = [P, P, i32, i32, i32, P]
         _lib = L
     return _lib
 
@@ -264,3 +265,17 @@ def partials_rows(enc: Encoded, z, xplanes, l: int = 8, rows=None):
 
 def max_threads() -> int:
     return int(lib().oracle_max_threads())
+
+
+def hadamard_rows(X, signs, b: int) -> np.ndarray:
+    """Randomized block Hadamard rotation along N (§4.5; reading A21): every block of b columns
+    of every row becomes H_b diag(signs) x / sqrt(b), fp64, plain O(b^2) definition."""
+    X = np.ascontiguousarray(np.asarray(X, np.float64))
+    rows, N = X.shape
+    assert N % b == 0 and b & (b - 1) == 0
+    sg = np.ascontiguousarray(np.asarray(signs, np.int8))
+    assert sg.shape == (N,)
+    Y = np.empty_like(X)
+    lib().oracle_hadamard_rows(_p(X), _p(Y), rows, N, b, _p(sg))
+    return Y
+

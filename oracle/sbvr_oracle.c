@@ -443,3 +443,30 @@ int oracle_max_threads(void) {
   return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------ randomized Hadamard rotation
+ * PAPER.md P:255 (§4.5): weights are rotated by a randomized Hadamard transform before quantization
+ * to Gaussianize them and suppress outliers.  Reading (A21): block-diagonal rotation along
+ * the inner dimension N with blocks of b = 2^k columns, Q = H_b D / sqrt(b), D = diag(signs) (the
+ * random +-1 draws are an input), H_b the Sylvester-Hadamard matrix, H_b[i][k] = (-1)^popcount(i & k).
+ * Plain definition: y[i] = sum_k H_b[i][k] * signs[k] * x[k] / sqrt(b), an O(b^2) matrix-vector
+ * product per block (no butterflies), fp64. */
+void oracle_hadamard_rows(const double* X, double* Y, int rows, int N, int b, const int8_t* signs) {
+  const double inv = 1.0 / sqrt((double)b);
+#pragma omp parallel for schedule(static)
+  for (long r = 0; r < rows; ++r) {
+    for (int blk = 0; blk < N / b; ++blk) {
+      const double* x = X + (size_t)r * N + (size_t)blk * b;
+      const int8_t* sg = signs + (size_t)blk * b;
+      double* y = Y + (size_t)r * N + (size_t)blk * b;
+      for (int i = 0; i < b; ++i) {
+        double acc = 0.0;
+        for (int k = 0; k < b; ++k) {
+          const double h = (__builtin_popcount((unsigned)(i & k)) & 1) ? -1.0 : 1.0;
+          acc += h * (double)sg[k] * x[k];
+        }
+        y[i] = acc * inv;
+      }
+    }
+  }
+}

@@ -80,9 +80,10 @@ def lib():
         L.sbvr_pack_canonical.argtypes = [i32, i32, i32, i32, P, P, P, P, P]
         L.sbvr_unpack_canonical.argtypes = [i32, i32, i32, i32, P, P, P, P, P]
         L.sbvr_fill_ratio_table.argtypes = [P, P]
+        L.sbvr_hadamard_rows.argtypes = [P, P, i32, i32, i32, i32, P, P]
         for name in ("sbvr_weights_bytes", "sbvr_encode_weights", "sbvr_encode_vector", "sbvr_gemv_workspace_bytes",
                      "sbvr_workspace_init", "sbvr_gemv", "sbvr_gemv_batched", "sbvr_gemv_ex", "sbvr_debug_partials",
-                     "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table"):
+                     "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -305,3 +306,16 @@ def algorithmic_bytes(M: int, N: int, K: int, act: str = "sbvr", l: int = 8, T: 
     """B = M N K/8 + 5 M N/G + x + 4 M (x = 2N fp16, or N l/8 + 4 N/G SBVR), per token for x/y."""
     x = 2 * N if act == "fp16" else N * l // 8 + 4 * (N // G)
     return M * N * K // 8 + 5 * M * (N // G) + T * (x + 4 * M)
+
+
+def hadamard_rows(X: torch.Tensor, signs: torch.Tensor, block: int = 128, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """sbvr_hadamard_rows (§4.5): randomized block Hadamard rotation of every row of X (fp32 or fp16,
+    [rows, N]) with the +-1 diagonal `signs` (int8 [N]); out may be X (in place)."""
+    assert X.dim() == 2 and X.is_contiguous() and signs.dtype == torch.int8 and signs.numel() == X.shape[1]
+    dt = {torch.float32: F32, torch.float16: F16}[X.dtype]
+    if out is None:
+        out = torch.empty_like(X)
+    _check(lib().sbvr_hadamard_rows(_ptr(X), _ptr(out), dt, X.shape[0], X.shape[1], block, _ptr(signs), _stream()),
+           "sbvr_hadamard_rows")
+    return out
+

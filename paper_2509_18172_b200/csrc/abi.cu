@@ -200,6 +200,17 @@ sbvr_status sbvr_gemv_batched(const sbvr_weights* w, const sbvr_act* X, int32_t 
   return sbvr_gemv_ex(w, X, T, Y, workspace, ws_bytes, SBVR_ALGO_AUTO, stream);
 }
 
+sbvr_status sbvr_hadamard_rows(const void* X, void* Y, int32_t dtype, int32_t rows, int32_t N, int32_t block,
+                               const int8_t* signs, void* stream) {
+  if (!X || !Y || !signs) return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  if (dtype != SBVR_F32 && dtype != SBVR_F16) return set_error(SBVR_ERR_UNSUPPORTED, "dtype %d (F32 or F16)", dtype);
+  if (block < 32 || block > 1024 || (block & (block - 1)))
+    return set_error(SBVR_ERR_UNSUPPORTED, "block %d: a power of two in 32..1024", block);
+  if (rows < 0 || N <= 0 || N % block) return set_error(SBVR_ERR_SHAPE, "rows=%d N=%d block=%d", rows, N, block);
+  if (!aligned16(X) || !aligned16(Y)) return set_error(SBVR_ERR_ALIGNMENT, "X/Y must be 16-byte aligned");
+  return launch_hadamard(X, Y, dtype, rows, N, block, signs, (cudaStream_t)stream);
+}
+
 sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_t algo, int32_t* P, void* stream) {
   sbvr_status s = check_weights(w);
   if (s != SBVR_OK) return s;

@@ -42,7 +42,10 @@
 namespace sbvr {
 namespace {
 
-constexpr int kImmaWarps = 16;       // warps per CTA (one CTA per SM: the register file is full)
+#ifndef SBVR_MMA_WARPS
+#define SBVR_MMA_WARPS 16
+#endif
+constexpr int kImmaWarps = SBVR_MMA_WARPS;   // warps per CTA (one CTA per SM: the register file is full)
 constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at least this many units per CTA
 constexpr int kSlots = 2;            // shared-memory ring depth per warp
 constexpr int kMaxTT = 4;            // tokens per pass (batched)
@@ -508,8 +511,8 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     if (!DEBUG && (!has_next || bn != b) && !(p.exp & 4)) {
       // warps of this CTA with tiles in band b: a contiguous run [wf, wl] (ballot over the warps)
       const unsigned int holders =
-          __ballot_sync(0xffffffffu, lane < kImmaWarps && s_fb[lane & (kImmaWarps - 1)] <= b &&
-                                         s_lb[lane & (kImmaWarps - 1)] >= b);
+          __ballot_sync(0xffffffffu, lane < kImmaWarps && s_fb[min(lane, kImmaWarps - 1)] <= b &&
+                                         s_lb[min(lane, kImmaWarps - 1)] >= b);
       const int wf = __ffs(holders) - 1, wl = 31 - __clz(holders);
       const bool shared = V0 > b * NG || V1 < min((b + 1) * NG, p.Us);    // other CTAs hold units of b
       float* sp = s_part + ((size_t)wib * 2 + (b == s_fb[wib] ? 0 : 1)) * (TT * 64);

@@ -84,5 +84,7 @@ sbvr_status launch_gemv_pipe(const sbvr_weights* w, const sbvr_act* x, float* y,
                              cudaStream_t st);
 size_t pipe_workspace_bytes(const sbvr_weights* w);
 bool pipe_supported(const sbvr_weights* w, const sbvr_act* x);
+sbvr_status launch_hadamard(const void* X, void* Y, int dtype, int rows, int N, int b, const int8_t* signs,
+                            cudaStream_t st);
 
 }  // namespace sbvr

@@ -30,6 +30,12 @@ def student_t_weight(M: int, N: int, seed: int, df: float = 3.0, sigma: float = 
     return (rng.standard_t(df, size=(M, N)) * sigma).astype(np.float32)
 
 
+def hadamard_signs(N: int, seed: int) -> np.ndarray:
+    """The random +-1 diagonal D of the randomized Hadamard rotation, int8 [N]."""
+    rng = np.random.default_rng(seed)
+    return np.where(rng.random(N) < 0.5, -1, 1).astype(np.int8)
+
+
 def activation(N: int, seed: int, T: int = 1, outliers: int = 0) -> np.ndarray:
     """x ~ N(0, 1) as fp16 [T][N] (post-RMSNorm scale); optional outlier channels x50."""
     g = torch.Generator().manual_seed(int(seed))

@@ -261,3 +261,48 @@ def test_abi_errors():
     y = sb.gemv(w, act)
     torch.cuda.synchronize()
     assert not y.any()                       # zero activation -> zero output
+
+
+# ------------------------------------------------------------------ f4: randomized Hadamard rotation
+@pytest.mark.parametrize("rows,N,b", [(1, 32, 32), (3, 256, 64), (17, 1024, 128), (5, 4096, 1024), (33, 14336, 512),
+                                      (2, 768, 256)])
+@pytest.mark.parametrize("dt", [torch.float32, torch.float16])
+def test_hadamard_rows(rows, N, b, dt):
+    """Tolerance: fp32 butterflies add at most log2(b) roundings per output (<= 10 x 2^-24 relative to
+    the block norm), so 1e-5 normwise; fp16 output rounding adds 2^-11 relative -> 1e-3."""
+    W = synthetic.student_t_weight(rows, N, seed=rows + N).astype(np.float32)
+    if dt == torch.float16:
+        W = W.astype(np.float16).astype(np.float32)
+    s = synthetic.hadamard_signs(N, seed=b)
+    X = torch.from_numpy(W).to(DEV).to(dt)
+    sg = torch.from_numpy(s).to(DEV)
+    Y = sb.hadamard_rows(X, sg, block=b)
+    Xi = X.clone()
+    sb.hadamard_rows(Xi, sg, block=b, out=Xi)            # in place
+    torch.cuda.synchronize()
+    ref = oracle.hadamard_rows(W.astype(np.float64), s, b)
+    err = np.abs(Y.double().cpu().numpy() - ref).max() / np.abs(ref).max()
+    assert err <= (1e-5 if dt == torch.float32 else 1e-3), err
+    assert torch.equal(Y, Xi)
+
+
+def test_hadamard_errors():
+    X = torch.zeros(2, 96, device=DEV)
+    sg = torch.ones(96, dtype=torch.int8, device=DEV)
+    with pytest.raises(sb.SbvrError) as e:
+        sb.hadamard_rows(X, sg, block=96)
+    assert e.value.status == sb.ERR_UNSUPPORTED
+    with pytest.raises(sb.SbvrError) as e:
+        sb.hadamard_rows(X, sg, block=64)
+    assert e.value.status == sb.ERR_SHAPE
+
+
+def test_hadamard_then_encode_lowers_heavy_tail_mse():
+    """f4's effect: encoding Student-t(3) weights after the 128-block rotation gives a lower mean
+    group MSE (the rotation is orthogonal, so the rotated-domain MSE is the original-domain MSE)."""
+    W = torch.from_numpy(synthetic.student_t_weight(64, 1024, seed=77)).to(DEV)
+    sg = torch.from_numpy(synthetic.hadamard_signs(1024, seed=78)).to(DEV)
+    _, mse0 = sb.encode_weights(W, K=4, n_scale=16, return_mse=True)
+    _, mse1 = sb.encode_weights(sb.hadamard_rows(W, sg, block=128), K=4, n_scale=16, return_mse=True)
+    torch.cuda.synchronize()
+    assert mse1.mean().item() < mse0.mean().item()
