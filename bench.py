@@ -480,7 +480,7 @@ def _time_gemv(sb, device, M, N, K, T, act_kind, algo, iters=60, seed=0):
     byts = sb.algorithmic_bytes(M, N, K, act=act_kind, l=L_BITS, T=T)
     del ws_, wsp
     torch.cuda.empty_cache()
-    return {"M": M, "N": N, "K": K, "T": T, "x": act_kind, "algo": {0: "auto", 1: "popc", 2: "tc", 3: "mma"}[algo],
+    return {"M": M, "N": N, "K": K, "T": T, "x": act_kind, "algo": {0: "auto", 1: "popc", 2: "tc", 3: "mma", 4: "pipe"}[algo],
             "us": round(us, 3), "GBps": round(byts / (us * 1e-6) / 1e9, 1)}
 
 
@@ -506,6 +506,64 @@ def sweeps(device):
             r = _time_gemv(sb, device, M, N, K_BITS, T, "fp16", sb.ALGO_AUTO)
             r["proj"] = name
             out["fp16x_llama3_8b"].append(r)
+    # config C3 on one GPU: the per-rank row shard of the Llama-3-70B MLP at P = 1, 2, 4, 8 (GEMV-only
+    # scaling; the y all-gather needs P GPUs and is timed by bench.py --gpus P)
+    out["llama3_70b_mlp_row_shards"] = []
+    for name, M, N in synthetic.LLAMA3_70B_MLP:
+        for P in (1, 2, 4, 8):
+            r = _time_gemv(sb, device, M // P, N, K_BITS, 1, "sbvr", sb.ALGO_AUTO, iters=40)
+            r.update(proj=name, P=P, M_full=M)
+            out["llama3_70b_mlp_row_shards"].append(r)
+    out["layer_chain_llama3_8b"] = layer_chain(sb, device)
+    return out
+
+
+def layer_chain(sb, device, reps=20):
+    """one synthetic Llama-3-8B decoder layer as deployed at batch 1 with every GEMV
+    converting its own input (sbvr_encode_vector + sbvr_gemv for q, k, v, o, gate, up, down -- unfused,
+    7 + 7 launches), one CUDA graph over a ring of layers (> L2), device time per layer (the TPOT-like
+    per-layer GEMV latency of Table 3's setting).  Also the fused form (qkv and gate_up stacked,
+    4 conversions) for comparison."""
+    out = {}
+    for label, mats in (("unfused_7", [(n, M, N) for n, M, N in synthetic.LLAMA3_8B_LAYER]),
+                        ("fused_4", [(n, M, N) for n, M, N, _, _ in FUSED])):
+        ring = 3
+        layers = []
+        for r in range(ring):
+            ws_ = []
+            for i, (n, M, N) in enumerate(mats):
+                pc, s16, b16, ri = synthetic.random_encoded(M, N, K_BITS, N_RATIO, seed=900 + 13 * r + i)
+                w = sb.pack_canonical(pc, s16, b16, ri, N_RATIO, device=device)
+                ws_.append((w, sb.Workspace.for_weights(w, 1), torch.empty(M, device=device),
+                            torch.from_numpy(synthetic.activation(N, seed=i)).to(device)))
+            layers.append(ws_)
+        acts = [[sb.encode_vector(x) for (_, _, _, x) in L] for L in layers]
+        stream = torch.cuda.Stream(device)
+        with torch.cuda.stream(stream):
+            def one(r):
+                for (w, wsp, y, x), a in zip(layers[r], acts[r]):
+                    sb.encode_vector(x, out=a)
+                    sb.gemv(w, a, y=y, ws=wsp)
+            for r in range(ring):
+                one(r)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(reps):
+                    one(i % ring)
+            g.replay()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g.replay()
+            b.record(stream)
+            torch.cuda.synchronize()
+        us = a.elapsed_time(b) * 1e3 / reps
+        byts = sum(sb.algorithmic_bytes(M, N, K_BITS, act="sbvr", l=L_BITS, T=1) for (_, M, N) in mats)
+        out[label] = {"us_per_layer": round(us, 2), "launches_per_layer": 2 * len(mats),
+                      "GBps": round(byts / (us * 1e-6) / 1e9, 1),
+                      "x32_layers_ms": round(32 * us / 1e3, 3)}
+        del layers, acts
+        torch.cuda.empty_cache()
     return out
 
 
