@@ -76,14 +76,17 @@ typedef enum { SBVR_F32 = 0, SBVR_F16 = 1, SBVR_BF16 = 2 } sbvr_dtype;
 typedef enum { SBVR_ACT_FP16 = 0, SBVR_ACT_SBVR = 1 } sbvr_act_kind;
 
 /* GEMV algorithm selector for sbvr_gemv_ex / sbvr_debug_partials.
- *  AUTO  : the fastest implemented kernel for the activation kind and batch (SBVR-x: MMA for
- *          T < 4, TC for T >= 4).
+ *  AUTO  : the fastest implemented kernel for the activation kind and batch (measured; SBVR-x: MMA,
+ *          which switches to its z-column form for T >= 3).
  *  POPC  : the paper's formulation, CUDA-core AND + __popc + coefficient FMAs.
  *  TC    : bit-sliced popcount on the 5th-generation tensor cores: A = plane & 0x01010101<<s in
  *          tensor memory, B = d_j bit-sliced x 2^(7-s) in shared memory, tcgen05.mma kind::i8
  *          M=128 N=8T K=32, which counts popc(beta_t & d_j) for 128 rows x 8 planes x T tokens.
  *  MMA   : the same bit-sliced popcount with warp-level mma.sync.m16n8k32.u8 (16 rows x 8 planes
- *          per instruction), the faster issue rate at batch 1.
+ *          per instruction), the faster issue rate at batch 1.  For T >= 3 SBVR-x tokens it uses the
+ *          z-column form: A = the plane bits themselves (u8 0/1), B = the tokens' int8 z = sum_j
+ *          alpha_j d_j (s8, 8 tokens as the 8 MMA columns), so the accumulator holds
+ *          T_t = sum_j alpha_j popc(beta_t & d_j) per token directly (same integers).
  *  PIPE  : the MMA formulation in a persistent warp-specialised kernel (producer warp + CTA-wide TMA
  *          ring, dynamically ticketed work items, deterministic split-K combine); batch 1, SBVR-x.
  *          Explicit only: measured slower than MMA on the Llama-3-8B step.          */

@@ -174,7 +174,8 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
   }
   if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, X, T, Y, nullptr, st);
   if (algo == SBVR_ALGO_AUTO)
-    algo = T < kTcMinT ? SBVR_ALGO_MMA : SBVR_ALGO_TC;   // PIPE is explicit-only (slower, profiles/r01_pipe_ab.txt)
+    algo = SBVR_ALGO_MMA;   // measured fastest at every T (z-column form from T = 3; profiles/r01_batched_zb.txt);
+                            // TC and PIPE are explicit-only
   if (algo == SBVR_ALGO_PIPE) {
     if (T != 1) return set_error(SBVR_ERR_UNSUPPORTED, "PIPE runs batch 1 (T=%d)", T);
     size_t need = pipe_workspace_bytes(w);

@@ -49,7 +49,8 @@ constexpr int kImmaWarps = SBVR_MMA_WARPS;   // warps per CTA (one CTA per SM: t
 constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at least this many units per CTA
 constexpr int kSlots = 2;            // shared-memory ring depth per warp
 constexpr int kMaxTT = 4;            // tokens per pass (batched)
-constexpr int kSumBatch = 8;         // CTA partials loaded per batch by a band's owner
+constexpr int kZbMinT = 3;           // SBVR-x batches from this T use the z-column formulation (8 tokens per pass)
+constexpr int kSumBatchMax = 8;      // CTA partials loaded per batch by a band's owner (x TT words per lane)
 constexpr unsigned int kSentinel = 0xFFFFFFFFu;   // "not yet written" (a NaN arithmetic never produces)
 
 struct ImmaParams {
@@ -123,6 +124,15 @@ __device__ __forceinline__ void mma_u8(int (&d)[4], uint32_t a0, uint32_t a1, ui
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
 }
 
+__device__ __forceinline__ void mma_u8s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1, int c0, int c1, int c2, int c3) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%11,%12,%13};"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "r"(c0), "r"(c1), "r"(c2), "r"(c3));
+}
+// w >> s for a compile-time s after unrolling, on the FMA pipe (IMAD.HI) instead of the ALU
+__device__ __forceinline__ uint32_t shr_u(uint32_t w, int s) { return s == 0 ? w : __umulhi(w, 1u << (32 - s)); }
+
 __device__ __forceinline__ void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                         uint32_t b0, uint32_t b1) {
   asm("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
@@ -195,11 +205,17 @@ __device__ __forceinline__ void issue_unit(uint8_t* slot, uint64_t* bar, const I
 // F16X: the fp16-x path (north star): M_t = sum_e beta_t[e] x_e with x in fp16, on
 // mma.m16n8k16 f16 (A = plane bits as 0/1.0 pairs, B = the lane's own x values, columns = tokens);
 // TT is then the number of token columns kept (<= 8).
-template <int K, int NB, int TT, bool DEBUG, bool F16X>
+template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB>
+#ifdef SBVR_MMA_MAXNREG
+__global__ void __maxnreg__(SBVR_MMA_MAXNREG) gemv_mma_kernel(ImmaParams p) {
+#else
 __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams p) {
+#endif
   using Gm = Geom<K, NB>;
-  constexpr int PT = (NB % 2 == 0 && TT == 1 && !F16X) ? 2 : 1;   // tiles per compute step
-  constexpr int NACC = F16X ? 2 : TT;                  // accumulators per tile: tokens (SBVR) or columns (F16X)
+  constexpr int PT = (NB % 2 == 0 && ((TT == 1 && !F16X) || ZB)) ? 2 : 1;   // tiles per compute step
+  constexpr int NACC = (F16X || ZB) ? 2 : TT;          // accumulators per tile: tokens (SBVR) or columns (F16X, ZB)
+  constexpr int NMMA = ZB ? 1 : TT;                    // MMAs per (tile, plane, slice pair)
+  constexpr int kSumBatch = kSumBatchMax / (TT >= 4 ? 4 : TT);   // keep the pulled words <= 16 per lane
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float s_rat[64];                 // r_i (fp32) for the Horner evaluation of sum_t r^t u_t
   __shared__ uint64_t s_bar[kImmaWarps][kSlots];
@@ -291,6 +307,17 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   uint32_t Xn[TT];
   float sxn[TT];
   uint4 Xh[F16X ? 4 : 1];                              // fp16-x: x[token gq][32c .. 32c+31] of the group
+  uint32_t Xz[ZB ? 8 : 1];                             // ZB: word c of the 8 planes of token gq (sign-extended)
+  float sxz[2];                                        // ZB: scales of this lane's output tokens 2c, 2c+1
+  auto load_xz = [&](int gg) {
+    if constexpr (ZB) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        Xz[j] = gq < p.ntok ? __ldg(p.xplanes + (((size_t)gq * NG + gg) * p.l + min(j, p.l - 1)) * 4 + c) : 0u;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) sxz[h] = 2 * c + h < p.ntok ? __ldg(p.xscales + (size_t)(2 * c + h) * NG + gg) : 0.f;
+    }
+  };
   auto load_xh = [&](int gg) {
     if constexpr (F16X) {
       if (gq < p.ntok) {
@@ -305,6 +332,8 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   };
   if constexpr (F16X) {
     load_xh(g);
+  } else if constexpr (ZB) {
+    load_xz(g);
   } else {
 #pragma unroll
     for (int tk = 0; tk < TT; ++tk) {
@@ -315,8 +344,9 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 
   for (int k = 0; k < n_mine; ++k) {
     // ---- B operand for group g: activation plane gq, word c, bit-sliced and pre-scaled by 2^(7-s)
-    uint32_t Bq[TT][4][2];
+    uint32_t Bq[NMMA][4][2];
     float sx[TT];
+    float sxc[2];
     uint32_t Bh[F16X ? 8 : 1][2];                       // fp16-x B: (x_s, x_16+s) pairs for s = 2m, 2m+1
     if constexpr (F16X) {
       const uint32_t xw[16] = {Xh[0].x, Xh[0].y, Xh[0].z, Xh[0].w, Xh[1].x, Xh[1].y, Xh[1].z, Xh[1].w,
@@ -326,6 +356,39 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
         Bh[m][0] = __byte_perm(xw[m], xw[8 + m], 0x5410);   // (x_2m, x_16+2m)
         Bh[m][1] = __byte_perm(xw[m], xw[8 + m], 0x7632);   // (x_2m+1, x_16+2m+1)
       }
+    } else if constexpr (ZB) {
+      // B = z (s8) of token gq, bytes ordered like the A slices: Bq[pr][h] byte i = z(32c + 8i + 2pr + h).
+      // The 8 plane words X_j (bit e = bit j of z_e) are an 8x8 bit matrix per byte lane; three
+      // delta-swap stages transpose it, so register s holds, in byte i, the bits j of element 8i + s.
+      uint32_t Z[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) Z[j] = Xz[j];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        const uint32_t t = ((Z[j] >> 1) ^ Z[j + 1]) & 0x55555555u;
+        Z[j + 1] ^= t;
+        Z[j] ^= t << 1;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (!(j & 2)) {
+          const uint32_t t = ((Z[j] >> 2) ^ Z[j + 2]) & 0x33333333u;
+          Z[j + 2] ^= t;
+          Z[j] ^= t << 2;
+        }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t t = ((Z[j] >> 4) ^ Z[j + 4]) & 0x0F0F0F0Fu;
+        Z[j + 4] ^= t;
+        Z[j] ^= t << 4;
+      }
+#pragma unroll
+      for (int pr = 0; pr < 4; ++pr) {
+        Bq[0][pr][0] = Z[2 * pr];
+        Bq[0][pr][1] = Z[2 * pr + 1];
+      }
+      sxc[0] = sxz[0];
+      sxc[1] = sxz[1];
     } else {
 #pragma unroll
       for (int tk = 0; tk < TT; ++tk) {
@@ -348,6 +411,8 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
       const int gp = has_next ? gn : g;
       if constexpr (F16X) {
         load_xh(gp);
+      } else if constexpr (ZB) {
+        load_xz(gp);
       } else {
 #pragma unroll
         for (int tk = 0; tk < TT; ++tk) {
@@ -434,7 +499,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
       }
 
       // ---- AND + popcount on the tensor pipe: PT x K independent chains (tile, plane) of 4 MMAs
-      int D[PT][TT][K][4];
+      int D[PT][NMMA][K][4];
 #pragma unroll
       for (int pr = 0; pr < 4; ++pr) {
         const uint32_t m0 = 0x01010101u << (2 * pr), m1 = 0x01010101u << (2 * pr + 1);
@@ -442,15 +507,34 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
         for (int t = 0; t < K; ++t)
 #pragma unroll
           for (int j = 0; j < PT; ++j) {
-            const uint32_t a0 = w[j][2 * t] & m0, a1 = w[j][2 * t + 1] & m0;
-            const uint32_t a2 = w[j][2 * t] & m1, a3 = w[j][2 * t + 1] & m1;
+            uint32_t a0, a1, a2, a3;
+            if constexpr (ZB) {
+              // A bytes are the bits themselves (0/1): shift on the FMA pipe (umulhi), mask on the ALU
+              a0 = shr_u(w[j][2 * t], 2 * pr) & 0x01010101u;
+              a1 = shr_u(w[j][2 * t + 1], 2 * pr) & 0x01010101u;
+              a2 = shr_u(w[j][2 * t], 2 * pr + 1) & 0x01010101u;
+              a3 = shr_u(w[j][2 * t + 1], 2 * pr + 1) & 0x01010101u;
+            } else {
+              a0 = w[j][2 * t] & m0;
+              a1 = w[j][2 * t + 1] & m0;
+              a2 = w[j][2 * t] & m1;
+              a3 = w[j][2 * t + 1] & m1;
+            }
 #pragma unroll
-            for (int tk = 0; tk < TT; ++tk) {
-              if (pr == 0)
-                mma_u8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], 0, 0, 0, 0);
-              else
-                mma_u8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], D[j][tk][t][0], D[j][tk][t][1],
-                       D[j][tk][t][2], D[j][tk][t][3]);
+            for (int tk = 0; tk < NMMA; ++tk) {
+              if constexpr (ZB) {
+                if (pr == 0)
+                  mma_u8s8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], 0, 0, 0, 0);
+                else
+                  mma_u8s8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], D[j][tk][t][0], D[j][tk][t][1],
+                           D[j][tk][t][2], D[j][tk][t][3]);
+              } else {
+                if (pr == 0)
+                  mma_u8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], 0, 0, 0, 0);
+                else
+                  mma_u8(D[j][tk][t], a0, a1, a2, a3, Bq[tk][pr][0], Bq[tk][pr][1], D[j][tk][t][0], D[j][tk][t][1],
+                         D[j][tk][t][2], D[j][tk][t][3]);
+              }
             }
           }
       }
@@ -468,6 +552,29 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
               if (j0 < p.l) dst[j0] = D[j][0][t][2 * h] >> 7;
               if (j1 < p.l) dst[j1] = D[j][0][t][2 * h + 1] >> 7;
             }
+        } else if constexpr (ZB) {
+          // D[j][0][t] = (T_t of rows gq, gq+8) for tokens 2c, 2c+1: sum_e beta_t[e] z_e, exact
+          const float2 s2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0[j] & 0xffffu))),
+                                        __half2float(__ushort_as_half((unsigned short)(sb1[j] & 0xffffu))));
+          const float2 b2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0[j] >> 16))),
+                                        __half2float(__ushort_as_half((unsigned short)(sb1[j] >> 16))));
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float2 Ph = __fadd2_rn(make_float2(__int_as_float(imad(D[j][0][K - 1][h], p.one, magic)),
+                                               __int_as_float(imad(D[j][0][K - 1][2 + h], p.one, magic))),
+                                   make_float2(-cmagic.x, -cmagic.y));
+            float2 U = Ph;
+#pragma unroll
+            for (int t = K - 2; t >= 0; --t) {
+              const float2 f = __fadd2_rn(make_float2(__int_as_float(imad(D[j][0][t][h], p.one, magic)),
+                                                      __int_as_float(imad(D[j][0][t][2 + h], p.one, magic))),
+                                          make_float2(-cmagic.x, -cmagic.y));
+              Ph = __ffma2_rn(Ph, r2[j], f);
+              U = __fadd2_rn(U, f);
+            }
+            const float2 v = __ffma2_rn(s2, Ph, __fmul2_rn(b2, U));
+            acc[h][i] = __ffma2_rn(make_float2(sxc[h], sxc[h]), v, acc[h][i]);
+          }
         } else {
           const float2 s2 = make_float2(__half2float(__ushort_as_half((unsigned short)(sb0[j] & 0xffffu))),
                                         __half2float(__ushort_as_half((unsigned short)(sb1[j] & 0xffffu))));
@@ -516,7 +623,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
       const int wf = __ffs(holders) - 1, wl = 31 - __clz(holders);
       const bool shared = V0 > b * NG || V1 < min((b + 1) * NG, p.Us);    // other CTAs hold units of b
       float* sp = s_part + ((size_t)wib * 2 + (b == s_fb[wib] ? 0 : 1)) * (TT * 64);
-      if constexpr (F16X) {
+      if constexpr (F16X || ZB) {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -578,7 +685,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int row = lane + 32 * h;
-              if (row < 16 * NB) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
+              if (row < 16 * NB && tk < p.ntok) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
             }
         } else {
           if (b == bA && V0 > b * NG) {
@@ -634,7 +741,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int row = lane + 32 * h;
-                if (row < 16 * NB) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
+                if (row < 16 * NB && tk < p.ntok) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
               }
           }
         }
@@ -703,12 +810,12 @@ size_t mma_workspace_bytes_(const sbvr_weights* w, int T) {
   return (size_t)C * TT * 64 * sizeof(float);
 }
 
-template <int K, int NB, int TT, bool DEBUG, bool F16X>
+template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB = false>
 static cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
   const int smem = kImmaWarps * Geom<K, NB>::kWarpBytes + kImmaWarps * 2 * TT * 64 * 4;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG, F16X>,
+    cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -723,11 +830,12 @@ static cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
   attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr_pdl;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG, F16X>, p);
+  return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB>, p);
 }
 
 template <int K, int NB>
-static cudaError_t launch_nb(const ImmaParams& p, int TT, bool debug, bool f16x, cudaStream_t st) {
+static cudaError_t launch_nb(const ImmaParams& p, int TT, bool debug, bool f16x, bool zb, cudaStream_t st) {
+  if (zb) return launch_one<K, NB, 8, false, false, true>(p, st);
   if (f16x) {
     switch (TT) {
       case 1: return launch_one<K, NB, 1, false, true>(p, st);
@@ -745,25 +853,25 @@ static cudaError_t launch_nb(const ImmaParams& p, int TT, bool debug, bool f16x,
 }
 
 template <int K>
-static cudaError_t launch_k(const ImmaParams& p, int NB, int TT, bool debug, bool f16x, cudaStream_t st) {
+static cudaError_t launch_k(const ImmaParams& p, int NB, int TT, bool debug, bool f16x, bool zb, cudaStream_t st) {
   switch (NB) {
-    case 4: return launch_nb<K, 4>(p, TT, debug, f16x, st);
-    case 3: return launch_nb<K, 3>(p, TT, debug, f16x, st);
-    case 2: return launch_nb<K, 2>(p, TT, debug, f16x, st);
-    default: return launch_nb<K, 1>(p, TT, debug, f16x, st);
+    case 4: return launch_nb<K, 4>(p, TT, debug, f16x, zb, st);
+    case 3: return launch_nb<K, 3>(p, TT, debug, f16x, zb, st);
+    case 2: return launch_nb<K, 2>(p, TT, debug, f16x, zb, st);
+    default: return launch_nb<K, 1>(p, TT, debug, f16x, zb, st);
   }
 }
 
-static cudaError_t launch_any(int K, const ImmaParams& p, int NB, int TT, bool debug, bool f16x, cudaStream_t st) {
+static cudaError_t launch_any(int K, const ImmaParams& p, int NB, int TT, bool debug, bool f16x, bool zb, cudaStream_t st) {
   switch (K) {
-    case 1: return launch_k<1>(p, NB, TT, debug, f16x, st);
-    case 2: return launch_k<2>(p, NB, TT, debug, f16x, st);
-    case 3: return launch_k<3>(p, NB, TT, debug, f16x, st);
-    case 4: return launch_k<4>(p, NB, TT, debug, f16x, st);
-    case 5: return launch_k<5>(p, NB, TT, debug, f16x, st);
-    case 6: return launch_k<6>(p, NB, TT, debug, f16x, st);
-    case 7: return launch_k<7>(p, NB, TT, debug, f16x, st);
-    default: return launch_k<8>(p, NB, TT, debug, f16x, st);
+    case 1: return launch_k<1>(p, NB, TT, debug, f16x, zb, st);
+    case 2: return launch_k<2>(p, NB, TT, debug, f16x, zb, st);
+    case 3: return launch_k<3>(p, NB, TT, debug, f16x, zb, st);
+    case 4: return launch_k<4>(p, NB, TT, debug, f16x, zb, st);
+    case 5: return launch_k<5>(p, NB, TT, debug, f16x, zb, st);
+    case 6: return launch_k<6>(p, NB, TT, debug, f16x, zb, st);
+    case 7: return launch_k<7>(p, NB, TT, debug, f16x, zb, st);
+    default: return launch_k<8>(p, NB, TT, debug, f16x, zb, st);
   }
 }
 
@@ -795,11 +903,15 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
   const uint32_t* xp = f16x ? nullptr : static_cast<const uint32_t*>(x->data);
   const uint16_t* xh = f16x ? static_cast<const uint16_t*>(x->data) : nullptr;
   const bool debug = P_debug != nullptr;
+  // SBVR-x batches: tokens as MMA columns, B = z (s8), A = the plane bits themselves (u8 0/1); one pass
+  // serves 8 tokens with T_t = sum_e beta_t[e] z_e read directly from the accumulator
+  static const int zb_min = getenv("SBVR_ZB_MIN_T") ? atoi(getenv("SBVR_ZB_MIN_T")) : kZbMinT;
+  const bool zb = !f16x && !debug && T >= zb_min;
   int done = 0;
   while (done < T) {
     const int rem = T - done;
     int TT;
-    if (f16x) TT = rem >= 8 ? 8 : (rem > 4 ? 8 : (rem > 2 ? 4 : rem));   // token columns of mma.m16n8k16
+    if (f16x || zb) TT = (zb || rem > 4) ? 8 : (rem > 2 ? 4 : rem);   // token columns of the MMA
     else TT = debug ? 1 : (rem >= 4 ? 4 : (rem >= 2 ? 2 : 1));
     const int ntok = rem < TT ? rem : TT;
     p.ntok = ntok;
@@ -816,7 +928,7 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
       p.Pw = part == 0 ? pl.C_main : pl.C_tail;
       p.qq = Us / p.Pw;
       p.rr = Us % p.Pw;
-      cudaError_t e = launch_any(w->K, p, NB, TT, debug, f16x, st);
+      cudaError_t e = launch_any(w->K, p, NB, TT, debug, f16x, zb, st);
       if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "gemv_mma setup: %s", cudaGetErrorString(e));
       sbvr_status s = check_launch("gemv_mma_kernel");
       if (s != SBVR_OK) return s;

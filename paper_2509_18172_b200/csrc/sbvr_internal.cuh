@@ -14,7 +14,6 @@ constexpr int kWPG = kG / 32;    // 32-bit words per plane per group
 constexpr int kTileRows = 16;    // rows per tile (mma m16)
 constexpr int kMaxK = 8;
 constexpr int kMaxT = 16;
-constexpr int kTcMinT = 4;     // AUTO: batches of >= 4 tokens go to the tensor-memory kernel
 
 // ------------------------------------------------------------------ device weight layout (sbvr.h)
 // One packed buffer of "units".  A unit is (row block rb of up to 128 rows, group g) stored as

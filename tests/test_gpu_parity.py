@@ -306,3 +306,39 @@ def test_hadamard_then_encode_lowers_heavy_tail_mse():
     _, mse1 = sb.encode_weights(sb.hadamard_rows(W, sg, block=128), K=4, n_scale=16, return_mse=True)
     torch.cuda.synchronize()
     assert mse1.mean().item() < mse0.mean().item()
+
+
+@pytest.mark.parametrize("T,l", [(3, 8), (8, 8), (8, 5), (11, 4), (16, 8)])
+def test_gemv_batched_z_columns(T, l):
+    """Batches on the z-column formulation (MMA path, T >= 3: B = z (s8) of 8 tokens, A = plane bits 0/1,
+    T_t read from the accumulator), incl. l < 8 (sign-extended planes) and a ragged last pass."""
+    M, N, K = 336, 640, 4
+    pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=T * 10 + l)
+    w = sb.pack_canonical(pc, s16, b16, ri, 16)
+    X = synthetic.activation(N, seed=T + l, T=T)
+    act = sb.encode_vector(torch.from_numpy(X).to(DEV), l=l)
+    Y = sb.gemv_ex(w, act, algo=sb.ALGO_MMA)
+    torch.cuda.synchronize()
+    enc = _oracle_encoded(pc, s16, b16, ri, K, 16)
+    for t in range(T):
+        z, xp, sc = oracle.encode_vector(X[t], 128, l)
+        assert_close(Y.cpu().numpy()[t], oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc)))
+
+
+@pytest.mark.parametrize("T", [3, 5, 6, 7, 9])
+@pytest.mark.parametrize("kind", ["sbvr", "fp16"])
+@pytest.mark.parametrize("algo", [sb.ALGO_AUTO, sb.ALGO_MMA, sb.ALGO_TC])
+def test_batched_writes_stay_inside_y(T, kind, algo):
+    """Passes that keep 8 (or 4) token columns must not write rows of Y beyond T."""
+    if kind == "fp16" and algo == sb.ALGO_TC:
+        pytest.skip("fp16-x runs on MMA/POPC")
+    M, N, K = 208, 512, 4
+    pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=T)
+    w = sb.pack_canonical(pc, s16, b16, ri, 16)
+    X = torch.from_numpy(synthetic.activation(N, seed=T, T=T)).to(DEV)
+    act = sb.encode_vector(X) if kind == "sbvr" else sb.fp16_activation(X)
+    big = torch.full((T + 8, M), 12345.0, device=DEV)
+    sb.gemv_ex(w, act, y=big[:T], algo=algo)
+    torch.cuda.synchronize()
+    assert torch.all(big[T:] == 12345.0)
+    assert torch.isfinite(big[:T]).all()
