@@ -618,9 +618,22 @@ def encode_throughput(device):
     torch.cuda.synchronize()
     s = a.elapsed_time(b) / 1e3
     groups = 4096 * 4096 // G
-    return {"shape": "4096x4096", "seconds": s, "groups_per_s": groups / s, "params_per_s": groups * G / s,
-            "search_space": "16x64x16 (R x S x B), strict fp64",
-            "full_llama3_8b_extrapolated_s": 54525952 / (groups / s)}
+    out = {"shape": "4096x4096", "seconds": s, "groups_per_s": groups / s, "params_per_s": groups * G / s,
+           "search_space": "16x64x16 (R x S x B), strict fp64",
+           "full_llama3_8b_extrapolated_s": 54525952 / (groups / s)}
+    # f2: the encode-time coefficient cache (per-row MRU cache of 8, moving-average admission)
+    _, m_full = sb.encode_weights(W[:512].contiguous(), K=K_BITS, return_mse=True)
+    a.record()
+    _, m_c, hit = sb.encode_weights_cached(W, K=K_BITS, cache_size=8, ema_alpha=0.1)
+    b.record()
+    torch.cuda.synchronize()
+    sc = a.elapsed_time(b) / 1e3
+    out["cached"] = {"cache_size": 8, "ema_alpha": 0.1, "seconds": sc, "groups_per_s": groups / sc,
+                     "speedup_vs_full_search": s / sc, "hit_rate": hit.float().mean().item(),
+                     "mean_mse_cached": m_c.mean().item(),
+                     "mean_mse_full_first512rows": m_full.mean().item(),
+                     "mean_mse_cached_first512rows": m_c[:512].mean().item()}
+    return out
 
 
 def measured_peak():

@@ -137,6 +137,19 @@ sbvr_status sbvr_weights_bytes(int32_t M, int32_t N, int32_t K, int32_t group_si
 sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, int32_t dtype, int32_t M,
                                 int32_t N, const sbvr_weights* out, double* group_mse, void* stream);
 
+/* sbvr_encode_weights_cached -- the encode-time coefficient cache of P:233 (§4.2 and its footnote):
+ * "we maintain a cache of previously selected variables r, s, and b ... check the cache ... before
+ * exploring the entire search space"; "if the error from the cached values is below this moving average
+ * [of the quantization error], the cached values are used".  Reading A22: per row, groups left to right
+ * (deterministic; rows run in parallel on the GPU), an MRU cache of up to cache_size (0..64) (r, s, b)
+ * triples, hit when the best cached MSE (strict '<', MRU order) < the moving average
+ * ema = (1-ema_alpha) ema + ema_alpha mse (initialised to the row's first full-search MSE); a miss runs
+ * Algorithm 1 exactly as sbvr_encode_weights and puts its winner in front.  Outputs as
+ * sbvr_encode_weights; group_hit (nullable, device, [M][N/G] uint8) = 1 for groups that took a cached set.
+ * cache_size = 0 gives exactly sbvr_encode_weights' result. */
+sbvr_status sbvr_encode_weights_cached(const sbvr_encode_config* cfg, int32_t cache_size, double ema_alpha,
+                                       const void* W, int32_t dtype, int32_t M, int32_t N, const sbvr_weights* out,
+                                       double* group_mse, uint8_t* group_hit, void* stream);
 /* sbvr_encode_vector -- P:235-243, Eq. 12.  x: device fp16 bits [T][N].  Per group of G:
  * s_x = absmax/(2^(l-1)-1) (fp32 IEEE), z = clamp(rne(x/s_x)), planes = l-bit two's
  * complement of z (plane l-1 = sign, weight -2^(l-1) s_x).  Outputs (device):

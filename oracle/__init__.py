@@ -84,6 +84,10 @@ def lib():
         L.oracle_partials_rows.argtypes = [P, P, P, i32, i32, i32, i32, P, i32, P, P]
         L.oracle_max_threads.restype = i32
         L.oracle_hadamard_rows.argtypes = [P, P, i32, i32, i32, P]
+        L.oracle_entry_mse.restype = f64
+        L.oracle_entry_mse.argtypes = [P, i32, i32, f64, f64, f64]
+        L.oracle_encode_matrix_cached.restype = i32
+        L.oracle_encode_matrix_cached.argtypes = [P, i32, i32, ctypes.POINTER(_Cfg), i32, f64, P, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -278,4 +282,31 @@ def hadamard_rows(X, signs, b: int) -> np.ndarray:
     Y = np.empty_like(X)
     lib().oracle_hadamard_rows(_p(X), _p(Y), rows, N, b, _p(sg))
     return Y
+
+
+def entry_mse(X, K: int, r: float, s: float, b: float) -> float:
+    """MSE of one group under the coefficient set c_t = s r^t + b (Eq. 4) with nearest-subset-sum
+    assignment -- the quantity Algorithm 1 minimises."""
+    X = np.ascontiguousarray(np.asarray(X, np.float64))
+    return lib().oracle_entry_mse(_p(X), X.size, K, float(r), float(s), float(b))
+
+
+def encode_matrix_cached(W, cfg: OracleConfig, cache_size: int = 8, alpha: float = 0.1):
+    """Encode with the encode-time coefficient cache (P:233 + footnote; reading A22): per row, groups
+    left to right, MRU cache of (r, s, b), hit when the best cached MSE < the moving average.
+    Returns (Encoded, hit[M][NG] uint8)."""
+    W = np.ascontiguousarray(np.asarray(W, np.float32))
+    M, N = W.shape
+    G, K = cfg.group_size, cfg.K
+    NG = N // G
+    planes = np.zeros((M, NG, K, G // 32), np.uint32)
+    s16 = np.zeros((M, NG), np.uint16)
+    b16 = np.zeros((M, NG), np.uint16)
+    ri = np.zeros((M, NG), np.uint8)
+    mse = np.zeros((M, NG), np.float64)
+    hit = np.zeros((M, NG), np.uint8)
+    c = cfg.c()
+    lib().oracle_encode_matrix_cached(_p(W), M, N, ctypes.byref(c), int(cache_size), float(alpha), _p(planes), _p(s16),
+                                      _p(b16), _p(ri), _p(mse), _p(hit))
+    return Encoded(M, N, cfg, planes, s16, b16, ri, mse), hit
 

@@ -310,6 +310,95 @@ int oracle_encode_matrix(const float* W, int M, int N, const oracle_cfg* cfg, ui
   return used;
 }
 
+/* ---------------------------------------------------------------- O-C encode-time coefficient cache
+ * P:233 (§4.2 and its footnote): "we maintain a cache of previously selected variables r, s, and b.
+ * The search algorithm first checks the cache to determine if any previously selected combinations
+ * ... provide sufficient accuracy before exploring the entire search space" -- footnote: "We maintain a
+ * moving average of the quantization error.  If the error from the cached values is below this moving
+ * average, the cached values are used."  Reading A22: the cache is per row, groups are
+ * visited left to right (a fixed order, so the result is deterministic and rows stay parallel); it holds
+ * up to `cache_size` (r index, s, b) triples in most-recently-used order; the best cached entry (strict
+ * '<' in MRU order) is used when its MSE is strictly below the moving average, which is initialised to
+ * the row's first full-search MSE and updated with every accepted MSE as ema = (1-alpha) ema + alpha mse;
+ * a hit moves the entry to the front, a miss runs Algorithm 1 and puts its winner in front (an identical
+ * triple already cached is moved instead of duplicated; the least recent entry falls out when full).     */
+double oracle_entry_mse(const double* X, int n, int K, double r, double s, double b) {
+  const int npts = 1 << K;
+  double c[OR_MAX_K], v[OR_MAX_PTS];
+  int32_t mk[OR_MAX_PTS];
+  oracle_coefficients(r, s, b, K, c);
+  oracle_subset_sums(c, K, v, mk);
+  double error_sum = 0.0;
+  for (int e = 0; e < n; ++e) {
+    double d = X[e] - v[oracle_nearest(v, npts, X[e])];
+    error_sum = error_sum + d * d;
+  }
+  return error_sum / (double)n;
+}
+
+int oracle_encode_matrix_cached(const float* W, int M, int N, const oracle_cfg* cfg, int cache_size, double alpha,
+                                uint32_t* planes, uint16_t* s16, uint16_t* b16, uint8_t* r_idx, double* mse,
+                                uint8_t* hit_out) {
+  const int G = cfg->group_size, NG = N / G, K = cfg->K, WPG = G / 32;
+  double R[256];
+  oracle_ratio_set(cfg->n_ratio, R);
+  long hits = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : hits)
+  for (long r = 0; r < M; ++r) {
+    int c_ri[64];
+    double c_s[64], c_b[64];
+    int n_c = 0, have_ema = 0;
+    double ema = 0.0;
+    for (int g = 0; g < NG; ++g) {
+      const long q = r * NG + g;
+      double X[OR_MAX_G];
+      for (int e = 0; e < G; ++e) X[e] = (double)W[r * (long)N + g * G + e];
+      int hit = 0, bidx = -1;
+      double best = INFINITY;
+      if (n_c > 0 && have_ema) {
+        for (int k = 0; k < n_c; ++k) {
+          double m = oracle_entry_mse(X, G, K, R[c_ri[k]], c_s[k], c_b[k]);
+          if (m < best) { best = m; bidx = k; }
+        }
+        if (best < ema) hit = 1;
+      }
+      int ri;
+      double sv, bv, m;
+      if (hit) {
+        ri = c_ri[bidx]; sv = c_s[bidx]; bv = c_b[bidx]; m = best;
+        for (int k = bidx; k > 0; --k) { c_ri[k] = c_ri[k - 1]; c_s[k] = c_s[k - 1]; c_b[k] = c_b[k - 1]; }
+      } else {
+        double Rr[256], S[4096], B[4096];
+        oracle_candidates(X, G, cfg, Rr, S, B);
+        int32_t bi, bj, bk;
+        m = oracle_search(X, G, K, Rr, cfg->n_ratio, S, cfg->n_scale, B, cfg->n_bias, &bi, &bj, &bk);
+        ri = bi; sv = S[bj]; bv = B[bk];
+        int at = -1;
+        for (int k = 0; k < n_c; ++k)
+          if (c_ri[k] == ri && c_s[k] == sv && c_b[k] == bv) { at = k; break; }
+        if (at < 0) {
+          if (n_c < cache_size) ++n_c;
+          at = n_c - 1;                      /* the least recent entry is overwritten when full */
+        }
+        for (int k = at; k > 0; --k) { c_ri[k] = c_ri[k - 1]; c_s[k] = c_s[k - 1]; c_b[k] = c_b[k - 1]; }
+      }
+      if (cache_size > 0) { c_ri[0] = ri; c_s[0] = sv; c_b[0] = bv; }
+      if (!have_ema) { ema = m; have_ema = 1; }
+      else ema = (1.0 - alpha) * ema + alpha * m;
+      double c[OR_MAX_K];
+      oracle_coefficients(R[ri], sv, bv, K, c);
+      oracle_assign(X, G, c, K, planes + q * (long)K * WPG);
+      s16[q] = oracle_fp16_bits(sv);
+      b16[q] = oracle_fp16_bits(bv);
+      r_idx[q] = (uint8_t)ri;
+      if (mse) mse[q] = m;
+      if (hit_out) hit_out[q] = (uint8_t)hit;
+      hits += hit;
+    }
+  }
+  return (int)hits;
+}
+
 /* ---------------------------------------------------------------- O-X activation conversion
  * §4.3 / Eq. 12: per vector (group of G, reading A12) scale
  * s_x = absmax / (2^(l-1) - 1) (reading A10), power-of-two coefficients

@@ -81,9 +81,10 @@ def lib():
         L.sbvr_unpack_canonical.argtypes = [i32, i32, i32, i32, P, P, P, P, P]
         L.sbvr_fill_ratio_table.argtypes = [P, P]
         L.sbvr_hadamard_rows.argtypes = [P, P, i32, i32, i32, i32, P, P]
+        L.sbvr_encode_weights_cached.argtypes = [P, i32, ctypes.c_double, P, i32, i32, i32, P, P, P, P]
         for name in ("sbvr_weights_bytes", "sbvr_encode_weights", "sbvr_encode_vector", "sbvr_gemv_workspace_bytes",
                      "sbvr_workspace_init", "sbvr_gemv", "sbvr_gemv_batched", "sbvr_gemv_ex", "sbvr_debug_partials",
-                     "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows"):
+                     "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows", "sbvr_encode_weights_cached"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -155,6 +156,24 @@ def encode_weights(W: torch.Tensor, K: int = 4, n_ratio: int = 16, n_scale: int 
     _check(lib().sbvr_encode_weights(ctypes.byref(cfg), _ptr(W), _DT[W.dtype], M, N, ctypes.byref(d), _ptr(mse),
                                      _stream()), "sbvr_encode_weights")
     return (w, mse) if return_mse else w
+
+
+def encode_weights_cached(W: torch.Tensor, K: int = 4, cache_size: int = 8, ema_alpha: float = 0.1, n_ratio: int = 16,
+                          n_scale: int = 64, n_bias: int = 16, s_min_factor: float = 2.0,
+                          out: Optional[SbvrWeights] = None):
+    """sbvr_encode_weights_cached: the encode-time coefficient cache.  Returns (weights, group
+    MSE [M, N/G] fp64, hit [M, N/G] uint8)."""
+    assert W.is_cuda and W.dim() == 2 and W.is_contiguous()
+    M, N = W.shape
+    w = out if out is not None else weights_empty(M, N, K, n_ratio, W.device)
+    cfg = _EncCfg(K, G, n_ratio, n_scale, n_bias, float(s_min_factor), 1)
+    mse = torch.empty((M, N // G), dtype=torch.float64, device=W.device)
+    hit = torch.empty((M, N // G), dtype=torch.uint8, device=W.device)
+    d = w.desc()
+    _check(lib().sbvr_encode_weights_cached(ctypes.byref(cfg), int(cache_size), float(ema_alpha), _ptr(W), _DT[W.dtype],
+                                            M, N, ctypes.byref(d), _ptr(mse), _ptr(hit), _stream()),
+           "sbvr_encode_weights_cached")
+    return w, mse, hit
 
 
 # ------------------------------------------------------------------ activations

@@ -100,8 +100,8 @@ sbvr_status sbvr_weights_bytes(int32_t M, int32_t N, int32_t K, int32_t group_si
   return SBVR_OK;
 }
 
-sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, int32_t dtype, int32_t M, int32_t N,
-                                const sbvr_weights* out, double* group_mse, void* stream) {
+static sbvr_status check_encode(const sbvr_encode_config* cfg, const void* W, int32_t dtype, int32_t M, int32_t N,
+                                const sbvr_weights* out) {
   if (!cfg || !W || !out) return set_error(SBVR_ERR_INVALID_ARG, "cfg/W/out is NULL");
   if (dtype != SBVR_F32 && dtype != SBVR_F16 && dtype != SBVR_BF16)
     return set_error(SBVR_ERR_INVALID_ARG, "unknown dtype %d", dtype);
@@ -115,9 +115,25 @@ sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, in
   if (out->M != M || out->N != N || out->K != cfg->K || out->group_size != cfg->group_size ||
       out->n_ratio != cfg->n_ratio)
     return set_error(SBVR_ERR_SHAPE, "output descriptor does not match M/N/K/group_size/n_ratio");
-  sbvr_status s = check_weights(out);
+  return check_weights(out);
+}
+
+sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, int32_t dtype, int32_t M, int32_t N,
+                                const sbvr_weights* out, double* group_mse, void* stream) {
+  sbvr_status s = check_encode(cfg, W, dtype, M, N, out);
   if (s != SBVR_OK) return s;
-  return launch_encode_weights(cfg, W, dtype, M, N, out, group_mse, (cudaStream_t)stream);
+  return launch_encode_weights(cfg, W, dtype, M, N, out, group_mse, -1, 0.0, nullptr, (cudaStream_t)stream);
+}
+
+sbvr_status sbvr_encode_weights_cached(const sbvr_encode_config* cfg, int32_t cache_size, double ema_alpha,
+                                       const void* W, int32_t dtype, int32_t M, int32_t N, const sbvr_weights* out,
+                                       double* group_mse, uint8_t* group_hit, void* stream) {
+  sbvr_status s = check_encode(cfg, W, dtype, M, N, out);
+  if (s != SBVR_OK) return s;
+  if (cache_size < 0 || cache_size > 64) return set_error(SBVR_ERR_INVALID_ARG, "cache_size=%d outside 0..64", cache_size);
+  if (!(ema_alpha > 0.0 && ema_alpha <= 1.0)) return set_error(SBVR_ERR_INVALID_ARG, "ema_alpha outside (0, 1]");
+  return launch_encode_weights(cfg, W, dtype, M, N, out, group_mse, cache_size, ema_alpha, group_hit,
+                               (cudaStream_t)stream);
 }
 
 sbvr_status sbvr_encode_vector(const uint16_t* x, int32_t T, int32_t N, int32_t group_size, int32_t l,

@@ -68,7 +68,8 @@ sbvr_status check_launch(const char* what);
 sbvr_status launch_encode_vector(const uint16_t* x, int T, int N, int l, uint32_t* planes, float* scales,
                                  cudaStream_t st);
 sbvr_status launch_encode_weights(const sbvr_encode_config* cfg, const void* W, int dtype, int M, int N,
-                                  const sbvr_weights* out, double* group_mse, cudaStream_t st);
+                                  const sbvr_weights* out, double* group_mse, int cache_size, double cache_alpha,
+                                  uint8_t* group_hit, cudaStream_t st);
 sbvr_status launch_ratio_table(float* ratio_pow, int n_ratio, int K, cudaStream_t st);
 sbvr_status launch_gemv_popc(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, int32_t* P_debug,
                              cudaStream_t st);

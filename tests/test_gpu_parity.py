@@ -342,3 +342,24 @@ def test_batched_writes_stay_inside_y(T, kind, algo):
     torch.cuda.synchronize()
     assert torch.all(big[T:] == 12345.0)
     assert torch.isfinite(big[:T]).all()
+
+
+# ------------------------------------------------------------------ f2: encode-time coefficient cache
+@pytest.mark.parametrize("K,cache_size,M,N", [(4, 8, 16, 1024), (3, 4, 16, 512), (2, 16, 32, 1024), (4, 0, 16, 512)])
+def test_encode_weights_cached_bitexact(K, cache_size, M, N):
+    """Planes, fp16 meta, ratio index, fp64 group MSE and the hit flags of the cached encoder equal the
+    oracle's (reading A22), incl. degenerate groups; cache_size 0 equals the uncached encoder."""
+    W = synthetic.with_degenerate_groups(synthetic.gaussian_weight(M, N, seed=K * 100 + M, sigma=0.02), seed=K)
+    cfg = oracle.OracleConfig(K=K, n_scale=16)
+    enc, hit = oracle.encode_matrix_cached(W, cfg, cache_size=cache_size, alpha=0.1)
+    w, mse, h = sb.encode_weights_cached(torch.from_numpy(W).to(DEV), K=K, cache_size=cache_size, ema_alpha=0.1,
+                                         n_scale=16)
+    torch.cuda.synchronize()
+    pc, s16, b16, ri = sb.unpack_canonical(w)
+    assert np.array_equal(h.cpu().numpy(), hit)
+    assert np.array_equal(pc, enc.planes) and np.array_equal(s16, enc.s16) and np.array_equal(b16, enc.b16)
+    assert np.array_equal(ri, enc.r_idx) and np.array_equal(mse.cpu().numpy(), enc.mse)
+    if cache_size == 0:
+        w0 = sb.encode_weights(torch.from_numpy(W).to(DEV), K=K, n_scale=16)
+        torch.cuda.synchronize()
+        assert torch.equal(w0.data, w.data)
