@@ -80,7 +80,15 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// Diagnostics (ablation switches, per-warp timestamps) exist only in a -DSBVR_DIAG build (tools/build_var.sh):
+// the production kernel carries no runtime checks for them.
+#ifdef SBVR_DIAG
 #define TSW(slot) do { if (p.ts && lane == 0) p.ts[((size_t)blockIdx.x * kImmaWarps + wib) * 8 + (slot)] = gtime(); } while (0)
+#define EXPM(bit) (p.exp & (bit))
+#else
+#define TSW(slot) do { } while (0)
+#define EXPM(bit) 0
+#endif
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -262,7 +270,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
     for (int s2 = 0; s2 < kSlots; ++s2)
-      if (s2 < n_mine && !(p.exp & 2)) issue_next(ring + s2 * Gm::kSlotBytes, bars + s2, s2);
+      if (s2 < n_mine && !EXPM(2)) issue_next(ring + s2 * Gm::kSlotBytes, bars + s2, s2);
   }
   for (int i = threadIdx.x; i < p.n_ratio; i += blockDim.x) s_rat[i] = K >= 2 ? p.ratio_pow[i * K + 1] : 0.f;
   for (int i = threadIdx.x; i < 2 * kImmaWarps; i += blockDim.x) s_cnt[i] = 0u;
@@ -275,7 +283,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   __syncthreads();
   if (n_mine <= 0) return;
   asm volatile("griddepcontrol.wait;" ::: "memory");   // activations / workspace / y only from here
-  if (p.exp & 8) return;
+  if (EXPM(8)) return;
 
   // lane constants (Eq. 12: alpha_j = 2^j, alpha_{l-1} = -2^(l-1); MMA columns j0 = 2c, j1 = 2c+1)
   const int j0 = 2 * c, j1 = 2 * c + 1;
@@ -423,14 +431,14 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     }
 
     uint8_t* sl = ring + slot * Gm::kSlotBytes;
-    if (!(p.exp & 2)) mbar_wait(bars + slot, phase);
+    if (!EXPM(2)) mbar_wait(bars + slot, phase);
     if (k == 0) TSW(1);
 
     // tiles are processed PT at a time so 4K independent MMA chains hide the IMMA latency; warp
     // tile ranges are PT-aligned, so a step's tiles are all in or all out of this warp's range
 #pragma unroll
     for (int ib = 0; ib < NB; ib += PT) {
-      if (ib < ti0 || ib >= ti1 || (p.exp & 1)) continue;   // not this warp's tiles (warp-uniform)
+      if (ib < ti0 || ib >= ti1 || EXPM(1)) continue;   // not this warp's tiles (warp-uniform)
       // lane (gq, c): word c of plane t of rows 16i+gq and 16i+gq+8 (row-major, chunk t at t ^ swz)
       uint32_t w[PT][2 * K];
       uint32_t sb0[PT], sb1[PT];
@@ -604,7 +612,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 
     // ---- release the slot and refill it with this warp's unit k + kSlots
     __syncwarp();
-    if (lane == 0 && k + kSlots < n_mine && !(p.exp & 2)) {
+    if (lane == 0 && k + kSlots < n_mine && !EXPM(2)) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue_next(sl, bars + slot, k + kSlots);
     }
@@ -615,7 +623,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     // quad-reduced partial in its smem slot (first / last band); the last warp of the CTA done
     // with the band (smem counter) sums the slots in warp order, then writes y or hands the CTA
     // partial to the band's last CTA.
-    if (!DEBUG && (!has_next || bn != b) && !(p.exp & 4)) {
+    if (!DEBUG && (!has_next || bn != b) && !EXPM(4)) {
       // warps of this CTA with tiles in band b: a contiguous run [wf, wl] (ballot over the warps)
       const unsigned int holders =
           __ballot_sync(0xffffffffu, lane < kImmaWarps && s_fb[min(lane, kImmaWarps - 1)] <= b &&
@@ -753,12 +761,14 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
     ++u;
   }
   TSW(3);
+#ifdef SBVR_DIAG
   if (p.ts && lane == 0) {
     unsigned int smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     p.ts[((size_t)blockIdx.x * kImmaWarps + wib) * 8 + 4] = smid;
     p.ts[((size_t)blockIdx.x * kImmaWarps + wib) * 8 + 5] = n_mine;
   }
+#endif
 }
 
 static int num_sms() {

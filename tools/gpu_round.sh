@@ -13,5 +13,10 @@ timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_d
   python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-cublas --no-encode > gpurun_out/bench_traffic.json 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_mma -s 2 -c 1 -o gpurun_out/prof_gateup \
   python tools/ncu_target.py --M 28672 --N 4096 > gpurun_out/ncu_full.log 2>&1
+# keep gpurun_out under the 64 MiB copy-back limit: export the report's raw page, drop the report
+ncu -i gpurun_out/prof_gateup.ncu-rep --page raw --csv > gpurun_out/prof_gateup_raw.csv 2>/dev/null
+ncu -i gpurun_out/prof_gateup.ncu-rep --page source --csv > gpurun_out/prof_gateup_source.csv 2>/dev/null
+mv gpurun_out/prof_gateup.ncu-rep /tmp/ 2>/dev/null
+du -sh gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi.txt 2>&1
 lscpu | grep -E "Model name|^CPU\(s\)" > gpurun_out/host.txt 2>&1; nproc >> gpurun_out/host.txt

@@ -1,4 +1,6 @@
-"""Per-warp timestamps of the batch-1 MMA GEMV inside a CUDA-graph chain (env SBVR_TS_PTR):
+"""(Needs the diagnostic build: `bash tools/build_var.sh diag -DSBVR_DIAG`, run with
+SBVR_LIB_AB=ab/libsbvr_diag.so -- the production kernel has no timestamp code.)
+Per-warp timestamps of the batch-1 MMA GEMV inside a CUDA-graph chain (env SBVR_TS_PTR):
 0 warp start, 1 first unit landed, 2 last unit computed, 3 exit (after band hand-off).
 Graph of 20 launches over distinct weight copies; stamps of the 10th launch (warm, PDL-overlapped).
 Prints percentiles over warps in us relative to the earliest start of that launch."""

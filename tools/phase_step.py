@@ -1,4 +1,6 @@
-"""Per-warp globaltimer stamps of the 4 GEMV launches of a bench step (qkv, o, gate_up, down) inside
+"""(Needs the diagnostic build: `bash tools/build_var.sh diag -DSBVR_DIAG`, run with
+SBVR_LIB_AB=ab/libsbvr_diag.so -- the production kernel has no timestamp code.)
+Per-warp globaltimer stamps of the 4 GEMV launches of a bench step (qkv, o, gate_up, down) inside
 a CUDA graph of 8 consecutive steps over a ring of 4 layers (as bench.py).  Env SBVR_TS_PTR gives each
 launch its own stamp buffer: 0 warp start, 1 first unit landed, 2 last unit computed, 3 exit, 4 smid.
 Prints, for step 5 of the graph, per launch the percentiles (us, relative to the step's first GEMV
