@@ -47,7 +47,10 @@ namespace {
 #endif
 constexpr int kImmaWarps = SBVR_MMA_WARPS;   // warps per CTA (one CTA per SM: the register file is full)
 constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at least this many units per CTA
-constexpr int kSlots = 2;            // shared-memory ring depth per warp
+#ifndef SBVR_MMA_SLOTS
+#define SBVR_MMA_SLOTS 2
+#endif
+constexpr int kSlots = SBVR_MMA_SLOTS;   // shared-memory ring depth per warp
 constexpr int kMaxTT = 4;            // tokens per pass (batched)
 constexpr int kZbMinT = 3;           // SBVR-x batches from this T use the z-column formulation (8 tokens per pass)
 constexpr int kSumBatchMax = 8;      // CTA partials loaded per batch by a band's owner (x TT words per lane)
