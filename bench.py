@@ -292,13 +292,21 @@ def run_sbvr(args, world, rank, local_rank, pg):
         plain_graphs[i % ring].replay()
     torch.cuda.synchronize()
     sampler = ClockSampler(local_rank) if rank == 0 else None
-    heat_end = time.time() + 0.6
-    i = 0
-    while time.time() < heat_end:
-        plain_graphs[i % ring].replay()
-        i += 1
-        if i % 200 == 0:
-            torch.cuda.synchronize()
+    # (with N > 1 ranks every step graph holds an NCCL all-gather, so every rank must replay the same
+    # number of steps: a fixed count, not a wall-clock deadline)
+    if world > 1:
+        for i in range(6000):
+            plain_graphs[i % ring].replay()
+            if i % 200 == 199:
+                torch.cuda.synchronize()
+    else:
+        heat_end = time.time() + 0.6
+        i = 0
+        while time.time() < heat_end:
+            plain_graphs[i % ring].replay()
+            i += 1
+            if i % 200 == 0:
+                torch.cuda.synchronize()
     torch.cuda.synchronize()
 
     # --- timed region: exactly K steps, barrier + sync on both sides
