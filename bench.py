@@ -71,58 +71,56 @@ class _Cudart:
         return ms.value
 
 
-# ------------------------------------------------------------------ clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------ clocks sampler (NVML, during the loaded region)
 class ClockSampler:
-    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clock, power and clock-event (throttle) reasons through NVML every `interval_s` from a
+    host thread while the GPU runs the heat-up and the timed steps (the timed region alone can be ~1 ms
+    at --steps 20, shorter than nvidia-smi's sampling period; NVML is polled directly)."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, device_index: int, interval_ms: int = 20):
-        self.rows = []
-        self.proc = None
+    def __init__(self, local_rank: int, interval_s: float = 0.001):
+        self.rows, self.h, self.max_sm = [], None, None
+        self._stop = threading.Event()
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(device_index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", str(interval_ms)],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [v for v in vis.split(",") if v.strip()]
+            idx = int(ids[local_rank]) if ids and all(v.strip().isdigit() for v in ids) else local_rank
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, args=(interval_s,), daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.h = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append((time.time(), line.strip()))
+    def _run(self, dt):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                self.rows.append((time.time(), sm, rs, pw))
+            except Exception:
+                pass
+            time.sleep(dt)
 
     def stop(self):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.h is not None:
+            self.t.join(timeout=2)
 
     def summary(self, t0: float, t1: float):
-        sm, mx, reasons, pw = [], None, set(), []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ts, line in self.rows:
-            if ts < t0 or ts > t1 + 0.05:
-                continue
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-                pw.append(float(parts[3]))
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
-                "power_w_max": max(pw) if pw else None}
+        rows = [r for r in self.rows if t0 <= r[0] <= t1 + 0.002]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_sm, "reasons": [], "samples": 0}
+        reasons = sorted({n for _, _, rs, _ in rows for bit, n in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": self.max_sm, "reasons": reasons,
+                "samples": len(rows), "sm_mhz_min": min(r[1] for r in rows), "power_w_max": max(r[3] for r in rows),
+                "window": "NVML, 1 ms period, over the clock heat-up and the timed steps"}
 
 
 # ------------------------------------------------------------------ workload
@@ -287,74 +285,80 @@ def run_sbvr(args, world, rank, local_rank, pg):
     step_bytes = step_gemv_bytes + step_conv_bytes
     rank_gemv_bytes = [gemv_bytes(sb, r1 - r0, N) for (_, M, N, r0, r1, w, ws, xin) in layers[0]]
 
-    # --- warmup + clock heat-up (untimed)
-    for i in range(max(args.warmup, 3)):
-        plain_graphs[i % ring].replay()
-    torch.cuda.synchronize()
-    sampler = ClockSampler(local_rank) if rank == 0 else None
-    # (with N > 1 ranks every step graph holds an NCCL all-gather, so every rank must replay the same
-    # number of steps: a fixed count, not a wall-clock deadline)
-    if world > 1:
-        for i in range(6000):
+    # Every replay below runs INSIDE `with torch.cuda.stream(stream)`: CUDAGraph.replay() launches on the
+    # current stream, and the timing events are recorded on that same stream, so they bracket the GPU
+    # work itself (round 1 replayed on the default stream while recording on `stream`, which timed only
+    # the host's enqueue rate).
+    with torch.cuda.stream(stream):
+        # --- warmup + clock heat-up (untimed)
+        for i in range(max(args.warmup, 3)):
             plain_graphs[i % ring].replay()
-            if i % 200 == 199:
-                torch.cuda.synchronize()
-    else:
-        heat_end = time.time() + 0.6
-        i = 0
-        while time.time() < heat_end:
-            plain_graphs[i % ring].replay()
-            i += 1
-            if i % 200 == 0:
-                torch.cuda.synchronize()
-    torch.cuda.synchronize()
-
-    # --- timed region: exactly K steps, barrier + sync on both sides
-    span_ms, span_n = 0.0, 0
-    pending = {}
-    if world > 1:
-        torch.distributed.barrier(group=pg)
-    torch.cuda.synchronize()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    wall0 = time.time()
-    t_start.record(stream)
-    for s in range(args.steps):
-        if s % EV_EVERY == EV_EVERY - 1:
-            gi = s % ring + ring * ((s // EV_EVERY) % 2)   # same layer as a plain step s: ring order kept
-            if gi in pending:                  # read the previous replay of this graph before reusing its events
-                span_ms += cr.elapsed_ms(*ev_graphs[gi][1])
-                span_n += 1
-            ev_graphs[gi][0].replay()
-            pending[gi] = True
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local_rank) if rank == 0 else None
+        wall_heat = time.time()
+        # (with N > 1 ranks every step graph holds an NCCL all-gather, so every rank must replay the same
+        # number of steps: a fixed count, not a wall-clock deadline)
+        if world > 1:
+            for i in range(6000):
+                plain_graphs[i % ring].replay()
+                if i % 200 == 199:
+                    torch.cuda.synchronize()
         else:
-            plain_graphs[s % ring].replay()
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    wall1 = time.time()
-    for gi in pending:
-        span_ms += cr.elapsed_ms(*ev_graphs[gi][1])
-        span_n += 1
-    if world > 1:
-        torch.distributed.barrier(group=pg)
-    elapsed = t_start.elapsed_time(t_end)
-    clocks = sampler.summary(wall0, wall1) if sampler else None
-    if sampler:
-        sampler.stop()
+            heat_end = time.time() + 0.6
+            i = 0
+            while time.time() < heat_end:
+                plain_graphs[i % ring].replay()
+                i += 1
+                if i % 200 == 0:
+                    torch.cuda.synchronize()
+        torch.cuda.synchronize()
 
-    # --- e2e: host (pinned) -> device inputs, kernels, device -> host outputs, every step
-    e2e_steps = args.steps
-    if world > 1:
-        torch.distributed.barrier(group=pg)
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for s in range(e2e_steps):
-        e2e_graphs[s % ring].replay()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
+        # --- timed region: exactly K steps, barrier + sync on both sides; an event after every step
+        span_ms, span_n = 0.0, 0
+        pending = {}
+        if world > 1:
+            torch.distributed.barrier(group=pg)
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        wall0 = time.time()
+        evs[0].record(stream)
+        for s in range(args.steps):
+            if s % EV_EVERY == EV_EVERY - 1:
+                gi = s % ring + ring * ((s // EV_EVERY) % 2)   # same layer as a plain step s: ring order kept
+                if gi in pending:                  # read the previous replay of this graph before reusing its events
+                    span_ms += cr.elapsed_ms(*ev_graphs[gi][1])
+                    span_n += 1
+                ev_graphs[gi][0].replay()
+                pending[gi] = True
+            else:
+                plain_graphs[s % ring].replay()
+            evs[s + 1].record(stream)
+        torch.cuda.synchronize()
+        wall1 = time.time()
+        for gi in pending:
+            span_ms += cr.elapsed_ms(*ev_graphs[gi][1])
+            span_n += 1
+        if world > 1:
+            torch.distributed.barrier(group=pg)
+        elapsed = evs[0].elapsed_time(evs[-1])
+        step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+        clocks = sampler.summary(wall_heat, wall1) if sampler else None
+        if sampler:
+            sampler.stop()
+
+        # --- e2e: host (pinned) -> device inputs, kernels, device -> host outputs, every step
+        e2e_steps = args.steps
+        if world > 1:
+            torch.distributed.barrier(group=pg)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for s in range(e2e_steps):
+            e2e_graphs[s % ring].replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1)
 
     # --- max over ranks
     t = torch.tensor([elapsed, e2e_ms], dtype=torch.float64, device=device)
@@ -365,15 +369,16 @@ def run_sbvr(args, world, rank, local_rank, pg):
     # per-GEMV breakdown (diagnostic, after the timed region): events between the launches
     per_gemv_ms = np.zeros(len(FUSED))
     n_split = 8 * ring
-    for i in range(n_split):
-        g, evs = split_graphs[i % ring]
-        g.replay()
-        torch.cuda.synchronize()
-        per_gemv_ms += [cr.elapsed_ms(a, b) for a, b in evs]
+    with torch.cuda.stream(stream):
+        for i in range(n_split):
+            g, gevs = split_graphs[i % ring]
+            g.replay()
+            torch.cuda.synchronize()
+            per_gemv_ms += [cr.elapsed_ms(a, b) for a, b in gevs]
     gemv_ms_avg = per_gemv_ms / n_split
     res = dict(elapsed=elapsed, e2e_ms=e2e_ms, step_bytes=step_bytes, step_gemv_bytes=step_gemv_bytes,
                gemv_ms_avg=gemv_ms_avg, rank_gemv_bytes=rank_gemv_bytes, clocks=clocks,
-               span_ms_avg=span_ms / max(span_n, 1), span_n=span_n)
+               span_ms_avg=span_ms / max(span_n, 1), span_n=span_n, step_ms=step_ms)
     h2d = sum(x.numel() * 2 for x in xs_host)
     d2h = sum(y.numel() * 4 for y in y_host)
     res["h2d"], res["d2h"] = h2d, d2h
@@ -734,6 +739,20 @@ def main():
             traffic = None
     e2e_val = res["step_bytes"] / (res["e2e_ms"] / K * 1e-3) / 1e9
     launches = K * (1 + len(FUSED))
+    sm = np.asarray(res["step_ms"]) * 1e3
+    step_stats = {"us_median": round(float(np.median(sm)), 3), "us_p10": round(float(np.percentile(sm, 10)), 3),
+                  "us_p90": round(float(np.percentile(sm, 90)), 3), "us_mean": round(float(sm.mean()), 3)}
+    # self-consistency of the headline (a number that fails one of these is not a measurement):
+    #  (1) a step cannot be shorter than the in-graph event span of the GEMV launches it contains;
+    #  (2) the step cannot move its algorithmic bytes faster than the HBM peak (+5 % for run-to-run);
+    #  (3) the end-to-end step (plus host<->device copies) cannot be shorter than the device-resident one.
+    checks = {"step_us_ge_gemv_span_us": [round(ms_per_step * 1e3, 3), round(res["span_ms_avg"] * 1e3, 3)],
+              "value_le_1.05_peak": [round(value, 1), round(1.05 * peak * world, 1)],
+              "e2e_step_ge_step_us": [round(res["e2e_ms"] / K * 1e3, 3), round(ms_per_step * 1e3, 3)]}
+    ok = (ms_per_step * 1e3 >= 0.99 * res["span_ms_avg"] * 1e3 and value <= 1.05 * peak * world
+          and res["e2e_ms"] / K >= 0.99 * ms_per_step)
+    if not ok:
+        raise SystemExit(f"bench self-check failed (timing does not bracket the GPU work): {checks}")
     out = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -774,6 +793,11 @@ def main():
                 "d2h_bytes_per_step": res["d2h"], "ms_per_step": round(res["e2e_ms"] / K, 5)},
         "gpu_launches": launches,
         "clocks": res["clocks"],
+        "step_us": step_stats,
+        "self_check": {"ok": True, **checks},
+        "timing": "CUDA events recorded on the replay stream after every one of the K graph replays (each replay "
+                  "and event runs under torch.cuda.stream(stream)); value = step algorithmic bytes x K / (last event "
+                  "- first event); barrier + synchronize on both sides; max over ranks",
     }
     if "standalone" in extra:
         out["us_per_gemv_standalone"] = extra["standalone"]

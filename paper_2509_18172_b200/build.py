@@ -50,12 +50,27 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def _obj_fresh(src: str) -> bool:
+    """An object is reusable when it is newer than its source and every shared header / this script."""
+    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+    if not os.path.exists(obj):
+        return False
+    shared = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(HERE, "..", "include", "sbvr.h"), __file__]
+    t = os.path.getmtime(obj)
+    return all(os.path.getmtime(d) <= t for d in [src] + shared)
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
+
+    def one(s):
+        obj = os.path.join(BUILD, os.path.basename(s) + ".o")
+        return obj if (not force and _obj_fresh(s)) else _compile(s, verbose)
+
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), sources()))
+        objs = list(ex.map(one, sources()))
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -461,6 +461,10 @@ __global__ void __launch_bounds__(NWG * 128 + 32, 1) gemv_tc_kernel(TcParams p) 
     const float* src = p.ws_part + ((size_t)(cta + 1) * NWG) * (TT * 128);
     for (int e = tid; e < nPre * TT * 128; e += blockDim.x) s_pre[e] = __ldcg(src + e);
     __syncthreads();
+    // back to rest (all 0xFF, sbvr_workspace_init): the workspace may be shared with kernels whose slots
+    // are sentinel-validated (PIPE)
+    for (int e = tid; e < nPre * TT * 128; e += blockDim.x)
+      reinterpret_cast<unsigned int*>(const_cast<float*>(src))[e] = 0xFFFFFFFFu;
     for (int q = tid; q < nPre; q += blockDim.x) p.ws_cnt[(cta + 1) * NWG + q] = 0xFFFFFFFFu;   // reset for the next launch
   }
   // ---- CTA combine in (group) order; row blocks we published are finished by their owner

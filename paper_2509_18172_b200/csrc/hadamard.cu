@@ -14,7 +14,7 @@ namespace sbvr {
 namespace {
 
 template <int M, bool HALF>
-__global__ void __launch_bounds__(256) hadamard_kernel(const void* __restrict__ X, void* Y, const int8_t* __restrict__ signs,
+__global__ void __launch_bounds__(256) hadamard_kernel(const void* X, void* Y, const int8_t* __restrict__ signs,
                                                        long n_blocks, int N, float scale) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
