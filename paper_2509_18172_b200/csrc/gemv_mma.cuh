@@ -200,6 +200,12 @@ struct Geom {
   static constexpr int kWarpBytes = kSlots * kSlotBytes;
 };
 
+__device__ __forceinline__ uint32_t ld_relaxed(const float* ptr) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int unit_owner(int v, int qq, int rr) {
   const int big = rr * (qq + 1);
   return v < big ? v / (qq + 1) : rr + (v - big) / qq;
@@ -731,13 +737,16 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
           // in its own slot (first / last band of the CTA), fences, and counts itself in on the band's
           // counter; the contributor that arrives last sums ALL slots in CTA order -- the same order
           // whoever arrives last, so y is deterministic -- writes y and re-arms slots and counter.
+          // (No memory fence: a fence makes every contributor wait for its stores to be acknowledged
+          // before counting itself in.  Instead the reducer validates each word against the at-rest
+          // sentinel -- the writers issued those stores before their atomic, so they land in bounded
+          // time and the reducer's wait never depends on another CTA making progress.)
           const int myslot = b == bA ? 0 : 1;
           float* part = p.ws_part + ((size_t)cta * 2 + myslot) * (TT * 64);
 #pragma unroll
           for (int tk = 0; tk < TT; ++tk)
 #pragma unroll
             for (int h = 0; h < 2; ++h) __stcg(part + tk * 64 + lane + 32 * h, v[tk][h]);
-          __threadfence();
           __syncwarp();
           const int c0 = unit_owner(b * NG, p.qq, p.rr);
           const int c1 = unit_owner(min((b + 1) * NG, p.Us) - 1, p.qq, p.rr);
@@ -747,22 +756,29 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
           // at rest the counter is 0xFFFFFFFF, so the k-th arrival (k = 1, 2, ...) reads k - 2 (mod 2^32)
           if (old + 2u == (unsigned int)(c1 - c0 + 1)) {
             TSW(7);
-            __threadfence();
             float sum[TT][2];
 #pragma unroll
             for (int tk = 0; tk < TT; ++tk) sum[tk][0] = sum[tk][1] = 0.f;
             for (int cb = c0; cb <= c1; cb += kSumBatch) {
-              float vals[kSumBatch][TT][2];
+              uint32_t vals[kSumBatch][TT][2];
+              for (long spins = 0;; ++spins) {       // reload the batch until no word is the sentinel
+                bool miss = false;
 #pragma unroll
-              for (int j = 0; j < kSumBatch; ++j) {
-                const int cc = cb + j;
-                const int fb = (cc * p.qq + min(cc, p.rr)) / NG;          // first band of CTA cc
-                const float* src = p.ws_part + ((size_t)cc * 2 + (b == fb ? 0 : 1)) * (TT * 64);
+                for (int j = 0; j < kSumBatch; ++j) {
+                  const int cc = cb + j;
+                  const int fb = (cc * p.qq + min(cc, p.rr)) / NG;          // first band of CTA cc
+                  const float* src = p.ws_part + ((size_t)cc * 2 + (b == fb ? 0 : 1)) * (TT * 64);
 #pragma unroll
-                for (int tk = 0; tk < TT; ++tk)
+                  for (int tk = 0; tk < TT; ++tk)
 #pragma unroll
-                  for (int h = 0; h < 2; ++h)
-                    vals[j][tk][h] = cc > c1 ? 0.f : cc == cta ? v[tk][h] : __ldcg(src + tk * 64 + lane + 32 * h);
+                    for (int h = 0; h < 2; ++h) {
+                      vals[j][tk][h] = cc > c1 ? 0u : cc == cta ? __float_as_uint(v[tk][h])
+                                                                : ld_relaxed(src + tk * 64 + lane + 32 * h);
+                      miss |= vals[j][tk][h] == kSentinel;
+                    }
+                }
+                if (!__any_sync(0xffffffffu, miss)) break;
+                if (spins > (1L << 26)) __trap();    // stores already issued never landed: fail loudly
               }
 #pragma unroll
               for (int j = 0; j < kSumBatch; ++j) {
@@ -770,7 +786,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 #pragma unroll
                 for (int tk = 0; tk < TT; ++tk)
 #pragma unroll
-                  for (int h = 0; h < 2; ++h) sum[tk][h] += vals[j][tk][h];
+                  for (int h = 0; h < 2; ++h) sum[tk][h] += __uint_as_float(vals[j][tk][h]);
               }
             }
             for (int cc = c0; cc <= c1; ++cc) {
