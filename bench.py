@@ -493,7 +493,7 @@ def _time_gemv(sb, device, M, N, K, T, act_kind, algo, iters=60, seed=0):
     byts = sb.algorithmic_bytes(M, N, K, act=act_kind, l=L_BITS, T=T)
     del ws_, wsp
     torch.cuda.empty_cache()
-    return {"M": M, "N": N, "K": K, "T": T, "x": act_kind, "algo": {0: "auto", 1: "popc", 2: "tc", 3: "mma", 4: "pipe"}[algo],
+    return {"M": M, "N": N, "K": K, "T": T, "x": act_kind, "algo": {0: "auto", 1: "popc", 2: "tc", 3: "mma", 4: "pipe", 5: "zt"}[algo],
             "us": round(us, 3), "GBps": round(byts / (us * 1e-6) / 1e9, 1)}
 
 
@@ -503,9 +503,11 @@ def sweeps(device):
     import paper_2509_18172_b200 as sb
     out = {"batched": [], "k_sweep_qwen25_7b": [], "fp16x_llama3_8b": []}
     for name, M, N in (("q_proj", 4096, 4096), ("gate_proj", 14336, 4096)):
-        for T in (1, 2, 4, 8, 16):
-            for algo in (sb.ALGO_MMA, sb.ALGO_TC):
-                r = _time_gemv(sb, device, M, N, K_BITS, T, "sbvr", algo)
+        for T in (1, 2, 4, 8, 16, 32, 64, 128, 256):
+            for algo in (sb.ALGO_ZT, sb.ALGO_MMA):
+                if algo == sb.ALGO_MMA and T > 16:
+                    continue
+                r = _time_gemv(sb, device, M, N, K_BITS, T, "sbvr", algo, iters=60 if T <= 64 else 20)
                 r["proj"] = name
                 out["batched"].append(r)
     for name, M, N in (("q_proj", 3584, 3584), ("gate_proj", 18944, 3584), ("down_proj", 3584, 18944)):

@@ -25,7 +25,7 @@ _lib = None
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_ALIGNMENT, ERR_CUDA, ERR_WORKSPACE = range(7)
 F32, F16, BF16 = 0, 1, 2
 ACT_FP16, ACT_SBVR = 0, 1
-ALGO_AUTO, ALGO_POPC, ALGO_TC, ALGO_MMA, ALGO_PIPE = 0, 1, 2, 3, 4
+ALGO_AUTO, ALGO_POPC, ALGO_TC, ALGO_MMA, ALGO_PIPE, ALGO_ZT = 0, 1, 2, 3, 4, 5
 G = 128
 
 
@@ -82,9 +82,11 @@ def lib():
         L.sbvr_fill_ratio_table.argtypes = [P, P]
         L.sbvr_hadamard_rows.argtypes = [P, P, i32, i32, i32, i32, P, P]
         L.sbvr_encode_weights_cached.argtypes = [P, i32, ctypes.c_double, P, i32, i32, i32, P, P, P, P]
+        L.sbvr_debug_zt_sums.argtypes = [P, P, i32, P, P]
         for name in ("sbvr_weights_bytes", "sbvr_encode_weights", "sbvr_encode_vector", "sbvr_gemv_workspace_bytes",
                      "sbvr_workspace_init", "sbvr_gemv", "sbvr_gemv_batched", "sbvr_gemv_ex", "sbvr_debug_partials",
-                     "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows", "sbvr_encode_weights_cached"):
+                     "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows", "sbvr_encode_weights_cached",
+                     "sbvr_debug_zt_sums"):
             getattr(L, name).restype = i32
         _lib = L
     return _lib
@@ -275,6 +277,16 @@ def debug_partials(w: SbvrWeights, x: SbvrActivation, algo: int = ALGO_TC) -> to
     _check(lib().sbvr_debug_partials(ctypes.byref(wd), ctypes.byref(xd), algo, _ptr(P), _stream()),
            "sbvr_debug_partials")
     return P
+
+
+def debug_zt_sums(w: SbvrWeights, x: SbvrActivation) -> torch.Tensor:
+    """Test-only: the exact integers T_t = sum_e beta_t[e] z_e of the tcgen05 z-column kernel, int32
+    [M, N/G, K, T] (sbvr_debug_zt_sums)."""
+    T = x.T
+    out = torch.full((w.M, w.N // G, w.K, T), -(2 ** 31), dtype=torch.int32, device=w.data.device)
+    wd, xd = w.desc(), x.desc()
+    _check(lib().sbvr_debug_zt_sums(ctypes.byref(wd), ctypes.byref(xd), T, _ptr(out), _stream()), "sbvr_debug_zt_sums")
+    return out
 
 
 # ------------------------------------------------------------------ host layout transforms

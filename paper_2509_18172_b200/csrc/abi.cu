@@ -47,7 +47,7 @@ static sbvr_status check_weights(const sbvr_weights* w) {
 
 static sbvr_status check_act(const sbvr_weights* w, const sbvr_act* x, int T) {
   if (!x || !x->data) return set_error(SBVR_ERR_INVALID_ARG, "activation descriptor/data is NULL");
-  if (T < 1 || T > kMaxT) return set_error(SBVR_ERR_SHAPE, "T=%d outside 1..16", T);
+  if (T < 1 || T > kMaxT) return set_error(SBVR_ERR_SHAPE, "T=%d outside 1..256", T);
   if (x->N != w->N) return set_error(SBVR_ERR_SHAPE, "x.N=%d != W.N=%d", x->N, w->N);
   if (x->group_size != w->group_size)
     return set_error(SBVR_ERR_SHAPE, "x.group_size=%d != W.group_size=%d", x->group_size, w->group_size);
@@ -147,12 +147,16 @@ sbvr_status sbvr_encode_vector(const uint16_t* x, int32_t T, int32_t N, int32_t 
 
 sbvr_status sbvr_gemv_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* bytes) {
   if (!w || !bytes) return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
-  if (T < 1 || T > kMaxT) return set_error(SBVR_ERR_SHAPE, "T=%d outside 1..16", T);
+  if (T < 1 || T > kMaxT) return set_error(SBVR_ERR_SHAPE, "T=%d outside 1..256", T);
   if (w->M <= 0 || w->N <= 0 || w->M % kTileRows || w->N % kG)
     return set_error(SBVR_ERR_SHAPE, "bad M/N %d/%d", w->M, w->N);
   const size_t a = tc_workspace_bytes(w, T), b = mma_workspace_bytes(w, T), c = pipe_workspace_bytes(w);
   *bytes = a > b ? a : b;
   if (c > *bytes) *bytes = c;
+  if (w->K <= 4) {
+    const size_t d = zt_workspace_bytes(w, T);
+    if (d > *bytes) *bytes = d;
+  }
   return SBVR_OK;
 }
 
@@ -186,12 +190,22 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
   if (algo == SBVR_ALGO_AUTO) {
     // diagnostics only (A/B timing in tools/): SBVR_FORCE_ALGO=<sbvr_algo> overrides AUTO for SBVR-x
     static const int forced = getenv("SBVR_FORCE_ALGO") ? atoi(getenv("SBVR_FORCE_ALGO")) : 0;
-    if (forced > 0 && forced <= SBVR_ALGO_PIPE && !(forced == SBVR_ALGO_PIPE && T != 1)) algo = forced;
+    if (forced > 0 && forced <= SBVR_ALGO_ZT && !(forced == SBVR_ALGO_PIPE && T != 1)) algo = forced;
   }
   if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, X, T, Y, nullptr, st);
-  if (algo == SBVR_ALGO_AUTO)
-    algo = SBVR_ALGO_MMA;   // measured fastest at every T (z-column form from T = 3; profiles/r01_batched_zb.txt);
-                            // TC and PIPE are explicit-only
+  if (algo == SBVR_ALGO_AUTO) {
+    // batches: the tcgen05 z-column kernel (one weight pass per 64 tokens) from zt_min tokens on; batch 1-2:
+    // the mma.sync bit-plane kernel.  SBVR_ZT_MIN_T overrides the switch point (A/B timing).
+    static const int zt_min = getenv("SBVR_ZT_MIN_T") ? atoi(getenv("SBVR_ZT_MIN_T")) : 12;
+    algo = (T >= zt_min && zt_supported(w, X)) ? SBVR_ALGO_ZT : SBVR_ALGO_MMA;
+  }
+  if (algo == SBVR_ALGO_ZT) {
+    if (!zt_supported(w, X)) return set_error(SBVR_ERR_UNSUPPORTED, "ZT needs an SBVR-x activation and K <= 4 (K=%d)", w->K);
+    size_t need = zt_workspace_bytes(w, T);
+    if (!workspace || ws_bytes < need)
+      return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    return launch_gemv_zt(w, X, T, Y, workspace, ws_bytes, nullptr, st);
+  }
   if (algo == SBVR_ALGO_PIPE) {
     if (T != 1) return set_error(SBVR_ERR_UNSUPPORTED, "PIPE runs batch 1 (T=%d)", T);
     size_t need = pipe_workspace_bytes(w);
@@ -241,6 +255,17 @@ sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_
     return launch_gemv_mma(w, x, 1, nullptr, nullptr, 0, P, (cudaStream_t)stream);
   if (algo == SBVR_ALGO_PIPE) return launch_gemv_pipe(w, x, nullptr, nullptr, P, (cudaStream_t)stream);
   return set_error(SBVR_ERR_INVALID_ARG, "bad algo %d", algo);
+}
+
+sbvr_status sbvr_debug_zt_sums(const sbvr_weights* w, const sbvr_act* x, int32_t T, int32_t* Tsum, void* stream) {
+  sbvr_status s = check_weights(w);
+  if (s != SBVR_OK) return s;
+  s = check_act(w, x, T);
+  if (s != SBVR_OK) return s;
+  if (!Tsum) return set_error(SBVR_ERR_INVALID_ARG, "Tsum is NULL");
+  if (T > 64) return set_error(SBVR_ERR_SHAPE, "T=%d: the debug export covers one pass (T <= 64)", T);
+  if (!zt_supported(w, x)) return set_error(SBVR_ERR_UNSUPPORTED, "ZT needs SBVR-x and K <= 4");
+  return launch_gemv_zt(w, x, T, nullptr, nullptr, 0, Tsum, (cudaStream_t)stream);
 }
 
 static sbvr_status check_pack_args(int32_t M, int32_t N, int32_t K, int32_t G) {

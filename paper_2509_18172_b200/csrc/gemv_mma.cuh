@@ -458,7 +458,6 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 
     // tiles are processed two at a time (PT = 2: 4K independent MMA chains hide the IMMA latency); a
     // warp range that starts or ends inside a pair takes that tile alone (PT = 1)
-#pragma unroll
     auto step = [&](auto ptc, const int ib) {
       constexpr int PT = decltype(ptc)::value;
 

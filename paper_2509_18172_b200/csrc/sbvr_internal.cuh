@@ -13,7 +13,7 @@ constexpr int kG = 128;          // group size supported by the kernels
 constexpr int kWPG = kG / 32;    // 32-bit words per plane per group
 constexpr int kTileRows = 16;    // rows per tile (mma m16)
 constexpr int kMaxK = 8;
-constexpr int kMaxT = 16;
+constexpr int kMaxT = 256;      // tokens per batched call (prefill chunks); kernels loop over passes
 
 // ------------------------------------------------------------------ device weight layout (sbvr.h)
 // One packed buffer of "units".  A unit is (row block rb of up to 128 rows, group g) stored as
@@ -84,6 +84,10 @@ sbvr_status launch_gemv_pipe(const sbvr_weights* w, const sbvr_act* x, float* y,
                              cudaStream_t st);
 size_t pipe_workspace_bytes(const sbvr_weights* w);
 bool pipe_supported(const sbvr_weights* w, const sbvr_act* x);
+sbvr_status launch_gemv_zt(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
+                           int32_t* T_debug, cudaStream_t st);
+size_t zt_workspace_bytes(const sbvr_weights* w, int T);
+bool zt_supported(const sbvr_weights* w, const sbvr_act* x);
 sbvr_status launch_hadamard(const void* X, void* Y, int dtype, int rows, int N, int b, const int8_t* signs,
                             cudaStream_t st);
 
