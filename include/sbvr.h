@@ -88,9 +88,9 @@ typedef enum { SBVR_ACT_FP16 = 0, SBVR_ACT_SBVR = 1 } sbvr_act_kind;
  *          alpha_j d_j (s8, 8 tokens as the 8 MMA columns), so the accumulator holds
  *          T_t = sum_j alpha_j popc(beta_t & d_j) per token directly (same integers).
  *  ZT    : batches on tcgen05 in the z-column form: A = the weight-plane bits as bytes 0/1 in tensor
- *          memory (M = 128 rows, K = 32 elements), B = the tokens' int8 z = sum_j alpha_j d_j (s8, N = up to 64
+ *          memory (M = 128 rows, K = 32 elements), B = the tokens' int8 z = sum_j alpha_j d_j (s8, N = up to 32
  *          tokens), kind::i8, so T_t = sum_e beta_t[e] z_e = sum_j alpha_j popc(beta_t & d_j) lands in tensor
- *          memory for 128 rows x N tokens per instruction; one weight pass per 64 tokens (tensor cores
+ *          memory for 128 rows x N tokens per instruction; one weight pass per 32 tokens (tensor cores
  *          amortise the weight decoding over the tokens).  SBVR-x, K <= 4.  AUTO picks it for T >= 12 (measured crossover vs MMA).
  *  PIPE  : the MMA formulation in a persistent warp-specialised kernel (producer warp + CTA-wide TMA
  *          ring, dynamically ticketed work items, deterministic split-K combine); batch 1, SBVR-x.
@@ -179,7 +179,7 @@ sbvr_status sbvr_gemv(const sbvr_weights* w, const sbvr_act* x, float* y, void* 
                       void* stream);
 
 /* sbvr_gemv_batched -- T (1..256) activation vectors in one descriptor (T decode streams, or a prefill chunk);
- * Y [T][M] fp32.  The kernels loop over token passes (ZT: 64 tokens per weight pass; MMA: 8). */
+ * Y [T][M] fp32.  The kernels loop over token passes (ZT: 32 tokens per weight pass; MMA: 8). */
 sbvr_status sbvr_gemv_batched(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
                               size_t ws_bytes, void* stream);
 
@@ -204,7 +204,7 @@ sbvr_status sbvr_hadamard_rows(const void* X, void* Y, int32_t dtype, int32_t ro
 sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_t algo, int32_t* P, void* stream);
 
 /* Test-only: the exact integers T_t = sum_e beta_t[e] z_e of the ZT kernel (before any float arithmetic),
- * int32 [M][N/G][K][T] row-major (device), SBVR-x activation with T (1..64) tokens. */
+ * int32 [M][N/G][K][T] row-major (device), SBVR-x activation with T (1..32) tokens. */
 sbvr_status sbvr_debug_zt_sums(const sbvr_weights* w, const sbvr_act* x, int32_t T, int32_t* Tsum, void* stream);
 
 /* Host-side layout transforms (host memory on both sides, no device work).  canonical planes

@@ -194,7 +194,7 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
   }
   if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, X, T, Y, nullptr, st);
   if (algo == SBVR_ALGO_AUTO) {
-    // batches: the tcgen05 z-column kernel (one weight pass per 64 tokens) from zt_min tokens on; batch 1-2:
+    // batches: the tcgen05 z-column kernel (one weight pass per 32 tokens) from zt_min tokens on; batch 1-2:
     // the mma.sync bit-plane kernel.  SBVR_ZT_MIN_T overrides the switch point (A/B timing).
     static const int zt_min = getenv("SBVR_ZT_MIN_T") ? atoi(getenv("SBVR_ZT_MIN_T")) : 12;
     algo = (T >= zt_min && zt_supported(w, X)) ? SBVR_ALGO_ZT : SBVR_ALGO_MMA;
@@ -263,7 +263,7 @@ sbvr_status sbvr_debug_zt_sums(const sbvr_weights* w, const sbvr_act* x, int32_t
   s = check_act(w, x, T);
   if (s != SBVR_OK) return s;
   if (!Tsum) return set_error(SBVR_ERR_INVALID_ARG, "Tsum is NULL");
-  if (T > 64) return set_error(SBVR_ERR_SHAPE, "T=%d: the debug export covers one pass (T <= 64)", T);
+  if (T > 32) return set_error(SBVR_ERR_SHAPE, "T=%d: the debug export covers one pass (T <= 32)", T);
   if (!zt_supported(w, x)) return set_error(SBVR_ERR_UNSUPPORTED, "ZT needs SBVR-x and K <= 4");
   return launch_gemv_zt(w, x, T, nullptr, nullptr, 0, Tsum, (cudaStream_t)stream);
 }

@@ -1,6 +1,6 @@
 // gemv_zt.cu -- SBVR GEMV for a batch of T tokens on the 5th-generation tensor cores (tcgen05.mma
 // kind::i8, accumulators in tensor memory): PAPER.md §4.4 for every token of the batch,
-// with one pass over the weights for up to 64 tokens (north star "batched (>1 token) variant ...
+// with one pass over the weights for up to 32 tokens (north star "batched (>1 token) variant ...
 // dense contraction", "leverage tensor cores ... amortizing the
 // dequantization overhead across multiple tokens").
 //
@@ -40,11 +40,13 @@ namespace zt {
 using namespace ptx;
 
 constexpr int kSlots = 4;          // TMA ring depth (unit records)
-constexpr int kWorkerWarps = 8;    // 2 per tensor-memory lane quarter
-constexpr int kIssuerWarps = 4;    // one per weight plane (K <= 4)
-constexpr int kThreads = (kWorkerWarps + kIssuerWarps + 1) * 32;
+constexpr int kExpandWarps = 16;   // A expansion (one plane each) + B build + coefficients: 4 per TMEM lane quarter
+constexpr int kEpiWarps = 8;       // epilogue (TMEM -> y) and split-K flush: 2 per lane quarter
+constexpr int kIssuerWarps = 4;    // MMA issue, one per weight plane (K <= 4)
+constexpr int kThreads = (kExpandWarps + kEpiWarps + kIssuerWarps) * 32;
+constexpr int kRing = 8;           // depth of the per-unit coefficient / token-scale ring (expansion -> epilogue)
 constexpr int kMaxPlanes = 4;
-constexpr int kMaxNT = 64;         // tokens per weight pass
+constexpr int kMaxNT = 32;         // tokens per weight pass
 constexpr unsigned int kSentinel = 0xFFFFFFFFu;
 
 struct ZtParams {
@@ -61,6 +63,9 @@ struct ZtParams {
   int Us, qq, rr;            // units, and their partition over CTAs
   unsigned long long* ts;    // diagnostics (-DSBVR_DIAG, env SBVR_TS_PTR): [CTA][32] per-phase SM-cycle totals
 };
+#ifndef ZT_ABL
+#define ZT_ABL 0   // ablation bits (diagnostic builds only): 1 no B build, 2 no A expansion, 4 no MMAs, 8 no x loads
+#endif
 #ifdef SBVR_DIAG
 // per-phase SM-cycle totals of one worker thread (warp 0, lane 0) and one issuer (warp 8) per CTA:
 // ts[CTA][0..15] worker phases, ts[CTA][16..31] issuer phases (tools/phase_zt.py)
@@ -95,24 +100,27 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
   constexpr int kUnitFull = 128 * (16 * K + 5);
   constexpr int kSlotBytes = (kUnitFull + 127) / 128 * 128;
   constexpr int kBBytes = 4 * NT * 32;           // B_q (q = 0..3): NT rows x 32 bytes each
-  constexpr int kHalf = NT / 2;                  // tokens per worker warp in the epilogue
+  constexpr int TQ = NT / 2;                     // tokens per epilogue warp (2 per lane quarter)
   constexpr int kDCol = 64 * K;                  // A_t[slot] at 64 t + 32 slot; D_t[buf] at kDCol + NT (t + K buf)
   // D double-buffered when it fits (MMA(k) need not wait for the epilogue of unit k-1)
   constexpr int kDBuf = kDCol + 2 * K * NT <= 512 ? 2 : 1;
-  constexpr int kPlanesLo = (K + 1) / 2;         // worker pair: planes [0, kPlanesLo) / [kPlanesLo, K)
+  constexpr int TC = TQ < 8 ? TQ : 8;            // epilogue token chunk (K x TC registers per TMEM load round)
   constexpr uint32_t kIdesc = (2u << 4) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) | (8u << 24);  // s32 += u8*s8, M=128
+  constexpr int kE = kExpandWarps, kP = kEpiWarps;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   uint8_t* sB = smem + kSlots * kSlotBytes;
+  float* s_c = reinterpret_cast<float*>(sB + 2 * kBBytes);      // [kRing][K][128] c_t = s r^t + b per row
   __shared__ float s_rpow[64 * kMaxPlanes];
   __shared__ __align__(8) uint64_t bar_full[kSlots];
-  __shared__ __align__(8) uint64_t bar_empty[kSlots];
   __shared__ __align__(8) uint64_t bar_a[2];
+  __shared__ __align__(8) uint64_t bar_abfree[2];   // MMAs of a unit done (all planes): its A/B slots are free
   __shared__ __align__(8) uint64_t bar_dfull[kMaxPlanes][2];
   __shared__ __align__(8) uint64_t bar_dempty[kMaxPlanes][2];
+  __shared__ unsigned int s_rel[kSlots];          // expansion warps done with a ring slot (the last refills it)
   __shared__ uint32_t s_tmem;
   __shared__ unsigned int s_old;
-  __shared__ float s_sx[4][kMaxNT];
+  __shared__ float s_sx[kRing][kMaxNT];           // token scales of a unit's group
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -128,20 +136,22 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
                           : p.units + (size_t)full_units * kUnitFull + (size_t)(u - full_units) * tail_ub;
   };
   auto unit_bytes = [&](int u) -> uint32_t { return u < full_units ? (uint32_t)kUnitFull : tail_ub; };
+  auto rows_of = [&](int rb) { return rb < p.n_full ? 128 : p.tail_rows; };
 
-  const int kProducer = kWorkerWarps + kIssuerWarps;
-  if (warp == kProducer && lane == 0) {
+  if (tid == (kE + kP) * 32) {                   // first issuer thread: barriers + the first copies
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&bar_full[s], 1);
-      mbar_init(&bar_empty[s], kWorkerWarps);
+      s_rel[s] = 0;
     }
-    for (int s = 0; s < 2; ++s) mbar_init(&bar_a[s], kWorkerWarps);
-    for (int t = 0; t < kMaxPlanes; ++t) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar_a[s], kE);
+      mbar_init(&bar_abfree[s], K);
+    }
+    for (int t = 0; t < kMaxPlanes; ++t)
       for (int b = 0; b < 2; ++b) {
         mbar_init(&bar_dfull[t][b], 1);
-        mbar_init(&bar_dempty[t][b], kWorkerWarps);
+        mbar_init(&bar_dempty[t][b], kP);
       }
-    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // weights are immutable: their copies start before the previous kernel has finished
     for (int s = 0; s < kSlots && s < n; ++s) {
@@ -156,183 +166,61 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
   tc_fence_after();
   const uint32_t tmem = s_tmem;
 
-  if (warp == kProducer) {
-    // ------------------------------------------------------------ producer: refill the ring
-    if (lane == 0) {
-      for (int k = kSlots; k < n; ++k) {
-        const int s = k % kSlots;
-        mbar_wait_sleep(&bar_empty[s], ((k / kSlots) - 1) & 1);
-        fence_proxy_async();
-        mbar_expect_tx(&bar_full[s], unit_bytes(V0 + k));
-        bulk_g2s(ring + s * kSlotBytes, unit_src(V0 + k), unit_bytes(V0 + k), &bar_full[s]);
-      }
-    }
-  } else if (warp >= kWorkerWarps) {
+  if (warp >= kE + kP) {
     // ------------------------------------------------------------ MMA issuer of plane t
-    const int t = warp - kWorkerWarps;
+    const int t = warp - (kE + kP);
     if (t < K && lane == 0) {
       PH_DECL
       const uint32_t bbase = smem_u32(sB);
       for (int k = 0; k < n; ++k) {
-        mbar_wait_sleep(&bar_a[k & 1], (k >> 1) & 1);             // A_t / B of unit k are in place
+        mbar_wait_backoff(&bar_a[k & 1], (k >> 1) & 1);         // A_t / B of unit k are in place
         PH(0);
         const int db = k % kDBuf;
-        if (k >= kDBuf)                                      // the epilogue has read D_t[db] of unit k - kDBuf
-          mbar_wait_sleep(&bar_dempty[t][db], ((k / kDBuf) - 1) & 1);
+        if (k >= kDBuf)                                          // the epilogue has read D_t[db] of unit k - kDBuf
+          mbar_wait_backoff(&bar_dempty[t][db], ((k / kDBuf) - 1) & 1);
         tc_fence_after();
         PH(1);
         const uint32_t tA = tmem + 64 * t + 32 * (k & 1);
         const uint32_t tD = tmem + kDCol + NT * (t + K * db);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          mma_i8_ts(tD, tA + 8 * q, smem_desc(bbase + (k & 1) * kBBytes + q * NT * 32, 128, 256), kIdesc, q);
+          if (!(ZT_ABL & 4)) mma_i8_ts(tD, tA + 8 * q, smem_desc(bbase + (k & 1) * kBBytes + q * NT * 32, 128, 256), kIdesc, q);
         mma_commit(&bar_dfull[t][db]);
+        mma_commit(&bar_abfree[k & 1]);
         PH(2);
       }
-      if (warp == kWorkerWarps) PH_DUMP(16);
+      if (t == 0) PH_DUMP(16);
     }
-  } else {
-    // ------------------------------------------------------------ workers (thread = row = TMEM lane)
-    asm volatile("griddepcontrol.wait;" ::: "memory");   // activations, workspace and Y from here on
+  } else if (warp < kE) {
+    // ------------------------------------------------------------ expansion warps (thread = row = TMEM lane)
+    // per unit: B (z of the group for NT tokens), A (this row's planes as bytes 0/1 -> TMEM), the row's
+    // coefficients c_t and the tokens' scales for the epilogue warps; then A/B ready -> the issuers
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // activations from here on
     PH_DECL
-    const int lq = warp & 3, th = warp >> 2;
+    const int lq = warp & 3, sub = warp >> 2;       // lane quarter; the plane this warp expands
     const int r = 32 * lq + lane;
     const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
     const int swz = chunk_swizzle(K, r);
-    const int t_lo = th == 0 ? 0 : kPlanesLo, t_hi = th == 0 ? kPlanesLo : K;
-    // B-build job of this thread: token bn, 32-element chunk bq of the group
-    const int bn = tid >> 2, bq = tid & 3;
-    const bool bjob = bn < NT;
+    const int bn = tid >> 2, bq = tid & 3;         // B-build job: token bn, 32-element chunk bq
+    const bool bwarp = warp * 8 < NT;             // warp-uniform: this warp has B-build jobs
     uint32_t X[8];
-    float sxn = 0.f;                                // token bn's scale for the group of X (bq == 0 threads)
+    float sxn = 0.f;
     auto load_x = [&](int g) {
+      if (bwarp) {
+        const bool live = bn < p.ntok;
+        const uint32_t* src = p.xplanes + ((size_t)bn * NG + g) * p.l * 4 + bq;
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        X[j] = (bjob && bn < p.ntok) ? __ldg(p.xplanes + (((size_t)bn * NG + g) * p.l + min(j, p.l - 1)) * 4 + bq) : 0u;
-      sxn = (!DEBUG && bjob && bq == 0 && bn < p.ntok) ? __ldg(p.xscales + (size_t)bn * NG + g) : 0.f;
-    };
-    float y[kHalf], accg[kHalf];
-#pragma unroll
-    for (int i = 0; i < kHalf; ++i) y[i] = 0.f;
-    float c_cur[K], c_nxt[K];
-
-    int rb_cur = -1, rows_cur = 0;
-
-    // leaving row block rb: write y (or hand the CTA partial to the last-arriving CTA of rb)
-    auto flush = [&](int rb, int rows) {
-      const bool shared = (long)rb * NG < V0 || (long)(rb + 1) * NG > V1;
-      if (!shared) {
-        if (!DEBUG && r < rows)
-#pragma unroll
-          for (int i = 0; i < kHalf; ++i) {
-            const int tok = th * kHalf + i;
-            if (tok < p.ntok) p.Y[(size_t)tok * p.M + (size_t)rb * 128 + r] = y[i];
-          }
-      } else if (!DEBUG) {
-        const int myslot = rb == V0 / NG ? 0 : 1;
-        float* part = p.ws_part + ((size_t)cta * 2 + myslot) * (NT * 128);
-#pragma unroll
-        for (int i = 0; i < kHalf; ++i) __stcg(part + (th * kHalf + i) * 128 + r, y[i]);
-        named_bar(1, kWorkerWarps * 32);
-        if (tid == 0) s_old = atomicAdd(p.ws_cnt + rb, 1u);
-        named_bar(1, kWorkerWarps * 32);
-        const int c0 = unit_cta(rb * NG, p.qq, p.rr), c1 = unit_cta((rb + 1) * NG - 1, p.qq, p.rr);
-        // at rest the counter is 0xFFFFFFFF: the k-th arrival reads k - 2 (mod 2^32)
-        if (s_old + 2u == (unsigned int)(c1 - c0 + 1)) {
-          float sum[kHalf];
-#pragma unroll
-          for (int i = 0; i < kHalf; ++i) sum[i] = 0.f;
-          for (int cc = c0; cc <= c1; ++cc) {
-            const int sl = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
-            float* src = p.ws_part + ((size_t)cc * 2 + sl) * (NT * 128);
-#pragma unroll
-            for (int i = 0; i < kHalf; ++i) {
-              float v = y[i];
-              if (cc != cta) {
-                uint32_t w;
-                long spins = 0;
-                while ((w = ld_relaxed_u32(src + (th * kHalf + i) * 128 + r)) == kSentinel)
-                  if (++spins > (1L << 26)) __trap();   // stores already issued never landed
-                v = __uint_as_float(w);
-              }
-              sum[i] += v;
-            }
-          }
-          for (int cc = c0; cc <= c1; ++cc) {
-            const int sl = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
-            unsigned int* dst = reinterpret_cast<unsigned int*>(p.ws_part) + ((size_t)cc * 2 + sl) * (NT * 128);
-#pragma unroll
-            for (int i = 0; i < kHalf; ++i) dst[(th * kHalf + i) * 128 + r] = kSentinel;
-          }
-          if (tid == 0) p.ws_cnt[rb] = kSentinel;
-          if (r < rows)
-#pragma unroll
-            for (int i = 0; i < kHalf; ++i) {
-              const int tok = th * kHalf + i;
-              if (tok < p.ntok) p.Y[(size_t)tok * p.M + (size_t)rb * 128 + r] = sum[i];
-            }
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < kHalf; ++i) y[i] = 0.f;
-    };
-
-    auto epilogue = [&](int k, int g, int rb, int rows) {
-      if (rb != rb_cur) {
-        PH(6);
-        if (rb_cur >= 0) flush(rb_cur, rows_cur);
-        PH(7);
-        rb_cur = rb;
-        rows_cur = rows;
-      }
-#pragma unroll
-      for (int t = 0; t < K; ++t) {
-        const int db = k % kDBuf;
-        PH(6);
-        mbar_wait_sleep(&bar_dfull[t][db], (k / kDBuf) & 1);
-        tc_fence_after();
-        PH(4);
-        uint32_t v[kHalf];
-        tmem_ld<kHalf>(tmem + lane_base + kDCol + NT * (t + K * db) + th * kHalf, v);
-        tmem_wait_ld();
-        pin<kHalf>(v);
-        PH(5);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar_dempty[t][db]);
-        if (DEBUG) {
-          if (r < rows)
-#pragma unroll
-            for (int i = 0; i < kHalf; ++i) {
-              const int tok = th * kHalf + i;
-              if (tok < p.ntok)
-                p.Tdbg[(((size_t)(rb * 128 + r) * NG + g) * K + t) * p.ntok + tok] = (int32_t)v[i];
-            }
-        } else {
-#pragma unroll
-          for (int i = 0; i < kHalf; ++i)
-            accg[i] = t == 0 ? c_cur[0] * __int2float_rn((int)v[i]) : fmaf(c_cur[t], __int2float_rn((int)v[i]), accg[i]);
-        }
-      }
-      if (!DEBUG) {
-#pragma unroll
-        for (int i = 0; i < kHalf; ++i) {
-          const int tok = th * kHalf + i;
-          y[i] = fmaf(s_sx[k & 3][th * kHalf + i], accg[i], y[i]);
-        }
+        for (int j = 0; j < 8; ++j) X[j] = live ? __ldg(src + min(j, p.l - 1) * 4) : 0u;
+        sxn = (!DEBUG && live && bq == 0) ? __ldg(p.xscales + (size_t)bn * NG + g) : 0.f;
       }
     };
-
     load_x(V0 % NG);
-    int kp_g = 0, kp_rb = 0, kp_rows = 0;           // unit k-1 (its epilogue runs after unit k's A/B)
+    int rb = V0 / NG, g = V0 - (V0 / NG) * NG;
     for (int k = 0; k < n; ++k) {
-      const int u = V0 + k;
-      const int rb = u / NG, g = u - rb * NG;
-      const int rows = rb < p.n_full ? 128 : p.tail_rows;
-      uint8_t* Bs = sB + (k & 1) * kBBytes;
-      // ---- B: z of the unit's group for NT tokens (slot k&1 was read by MMA(k-2), complete: the
-      // epilogue of unit k-2 waited for it)
-      if (bjob) {
+      const int rows = rows_of(rb);
+      if (k >= 2) mbar_wait_backoff(&bar_abfree[k & 1], ((k - 2) >> 1) & 1);   // A_t[k&1], B[k&1] read by MMA(k-2)
+      PH(0);
+      if (bwarp && !(ZT_ABL & 1)) {
         uint32_t Z[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) Z[j] = X[j];
@@ -356,35 +244,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
           Z[j] ^= x << 4;
         }
         // register s, byte i = z(32 bq + 8 i + s) = k-order byte 4 s + i of B row bn (MMA q = bq)
-        uint8_t* row = Bs + bq * (NT * 32) + (bn >> 3) * 256 + (bn & 7) * 16;
+        uint8_t* row = sB + (k & 1) * kBBytes + bq * (NT * 32) + (bn >> 3) * 256 + (bn & 7) * 16;
         *reinterpret_cast<uint4*>(row) = make_uint4(Z[0], Z[1], Z[2], Z[3]);
         *reinterpret_cast<uint4*>(row + 128) = make_uint4(Z[4], Z[5], Z[6], Z[7]);
+        if (bq == 0) s_sx[k % kRing][bn] = sxn;
       }
-      // token scales of this unit's group, read by its epilogue one iteration later (ring of 4: a worker warp
-      // can run at most one unit ahead of another -- each epilogue waits for MMAs that needed every warp)
-      if (bjob && bq == 0) s_sx[k & 3][bn] = sxn;
-      if (k + 1 < n) load_x((u + 1) % NG);
-      // ---- A: this row's planes as bytes 0/1 -> TMEM (A_t[k&1]); the element of column 8q + s,
-      // byte i is 32 q + 8 i + s, matching B's k order
-      const int slot = k % kSlots;
-      PH(0);
-      mbar_wait_sleep(&bar_full[slot], (k / kSlots) & 1);
+      const int g_next = g + 1 == NG ? 0 : g + 1;
+      if (k + 1 < n && !(ZT_ABL & 8)) load_x(g_next);
       PH(1);
+      const int slot = k % kSlots;
+      mbar_wait(&bar_full[slot], (k / kSlots) & 1);
+      PH(2);
       const uint8_t* sl = ring + slot * kSlotBytes;
-#pragma unroll
-      for (int t = 0; t < K; ++t) {
-        if (t < t_lo || t >= t_hi) continue;
-        const uint4 w4 = *reinterpret_cast<const uint4*>(sl + r * 16 * K + 16 * (t ^ swz));
+      if (sub < K && !(ZT_ABL & 2)) {
+        const uint4 w4 = *reinterpret_cast<const uint4*>(sl + r * 16 * K + 16 * (sub ^ swz));
         const uint32_t wq[4] = {w4.x, w4.y, w4.z, w4.w};
         uint32_t a[32];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
 #pragma unroll
           for (int s = 0; s < 8; ++s) a[8 * q + s] = shr_fma(wq[q], s) & 0x01010101u;
-        tmem_st32(tmem + lane_base + 64 * t + 32 * (k & 1), a);
+        tmem_st32(tmem + lane_base + 64 * sub + 32 * (k & 1), a);
       }
-      // ---- this row's coefficients c_t = s r^t + b (Eq. 4) for the epilogue
-      {
+      if (sub == K - 1) {                            // c_t = s r^t + b (Eq. 4) of this row, for the epilogue
         uint32_t sbw = 0, ri = 0;
         if (r < rows) {
           sbw = *reinterpret_cast<const uint32_t*>(sl + rows * 16 * K + 4 * r);
@@ -393,34 +275,160 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
         const float s_ = __half2float(__ushort_as_half((unsigned short)(sbw & 0xffffu)));
         const float b_ = __half2float(__ushort_as_half((unsigned short)(sbw >> 16)));
 #pragma unroll
-        for (int t = 0; t < K; ++t) c_nxt[t] = fmaf(s_, s_rpow[ri * K + t], b_);
+        for (int t = 0; t < K; ++t) s_c[((k % kRing) * K + t) * 128 + r] = fmaf(s_, s_rpow[ri * K + t], b_);
       }
-      PH(2);
+      PH(3);
       tmem_wait_st();
-      fence_proxy_async();              // B (generic stores) -> the MMA (async proxy)
+      fence_proxy_async();              // B (generic stores) -> the MMA (async proxy); slot reads -> the refill
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&bar_empty[slot]);
         mbar_arrive(&bar_a[k & 1]);
+        // the last expansion warp done with this slot refills it with unit k + kSlots
+        if (atomicAdd(&s_rel[slot], 1u) == kE - 1) {
+          s_rel[slot] = 0;
+          if (k + kSlots < n) {
+            mbar_expect_tx(&bar_full[slot], unit_bytes(V0 + k + kSlots));
+            bulk_g2s(ring + slot * kSlotBytes, unit_src(V0 + k + kSlots), unit_bytes(V0 + k + kSlots), &bar_full[slot]);
+          }
+        }
       }
-      PH(3);
-      // ---- epilogue of unit k-1 (its MMAs overlap this unit's A/B build)
-      if (k > 0) epilogue(k - 1, kp_g, kp_rb, kp_rows);
+      PH(4);
+      g = g_next;
+      if (g == 0) ++rb;
+    }
+    if (warp == 0) PH_DUMP(0);
+  } else {
+    // ------------------------------------------------------------ epilogue warps (thread = row = TMEM lane)
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // workspace and Y from here on
+    PH_DECL
+    const int ew = warp - kE;
+    const int lq = warp & 3, th = ew >> 2;           // lane quarter; token half
+    const int r = 32 * lq + lane;
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    const int etid = ew * 32 + lane;                  // 0 .. 255
+    float y[TQ];
+#pragma unroll
+    for (int i = 0; i < TQ; ++i) y[i] = 0.f;
+
+    // leaving row block rb: write y (or hand the CTA partial to the last-arriving CTA of rb)
+    auto flush = [&](int rb, int rows) {
+      const bool shared = (long)rb * NG < V0 || (long)(rb + 1) * NG > V1;
+      if (!shared) {
+        if (!DEBUG && r < rows)
+#pragma unroll
+          for (int i = 0; i < TQ; ++i) {
+            const int tok = th * TQ + i;
+            if (tok < p.ntok) p.Y[(size_t)tok * p.M + (size_t)rb * 128 + r] = y[i];
+          }
+      } else if (!DEBUG) {
+        const int myslot = rb == V0 / NG ? 0 : 1;
+        float* part = p.ws_part + ((size_t)cta * 2 + myslot) * (NT * 128);
+#pragma unroll
+        for (int i = 0; i < TQ; ++i) __stcg(part + (th * TQ + i) * 128 + r, y[i]);
+        named_bar(1, kP * 32);
+        if (etid == 0) s_old = atomicAdd(p.ws_cnt + rb, 1u);
+        named_bar(1, kP * 32);
+        const int c0 = unit_cta(rb * NG, p.qq, p.rr), c1 = unit_cta((rb + 1) * NG - 1, p.qq, p.rr);
+        // at rest the counter is 0xFFFFFFFF: the k-th arrival reads k - 2 (mod 2^32)
+        if (s_old + 2u == (unsigned int)(c1 - c0 + 1)) {
+          float sum[TQ];
+#pragma unroll
+          for (int i = 0; i < TQ; ++i) sum[i] = 0.f;
+          for (int cc = c0; cc <= c1; ++cc) {
+            const int sl = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
+            float* src = p.ws_part + ((size_t)cc * 2 + sl) * (NT * 128);
+#pragma unroll
+            for (int i = 0; i < TQ; ++i) {
+              float v = y[i];
+              if (cc != cta) {
+                uint32_t w;
+                long spins = 0;
+                while ((w = ld_relaxed_u32(src + (th * TQ + i) * 128 + r)) == kSentinel)
+                  if (++spins > (1L << 26)) __trap();   // stores already issued never landed
+                v = __uint_as_float(w);
+              }
+              sum[i] += v;
+            }
+          }
+          for (int cc = c0; cc <= c1; ++cc) {
+            const int sl = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
+            unsigned int* dst = reinterpret_cast<unsigned int*>(p.ws_part) + ((size_t)cc * 2 + sl) * (NT * 128);
+#pragma unroll
+            for (int i = 0; i < TQ; ++i) dst[(th * TQ + i) * 128 + r] = kSentinel;
+          }
+          if (etid == 0) p.ws_cnt[rb] = kSentinel;
+          if (r < rows)
+#pragma unroll
+            for (int i = 0; i < TQ; ++i) {
+              const int tok = th * TQ + i;
+              if (tok < p.ntok) p.Y[(size_t)tok * p.M + (size_t)rb * 128 + r] = sum[i];
+            }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < TQ; ++i) y[i] = 0.f;
+    };
+
+    int rb = V0 / NG, g = V0 - (V0 / NG) * NG, rb_cur = rb;
+    for (int k = 0; k < n; ++k) {
+      const int rows = rows_of(rb);
+      if (rb != rb_cur) {
+        PH(6);
+        flush(rb_cur, rows_of(rb_cur));
+        PH(7);
+        rb_cur = rb;
+      }
+      const int db = k % kDBuf;
       PH(6);
 #pragma unroll
-      for (int t = 0; t < K; ++t) c_cur[t] = c_nxt[t];
-
-      kp_g = g;
-      kp_rb = rb;
-      kp_rows = rows;
+      for (int t = 0; t < K; ++t) mbar_wait_backoff(&bar_dfull[t][db], (k / kDBuf) & 1);
+      tc_fence_after();
+      PH(4);
+      // token chunks of TC columns: all K planes of a chunk are loaded before one tcgen05.wait::ld
+#pragma unroll
+      for (int c0 = 0; c0 < TQ; c0 += TC) {
+        uint32_t v[K][TC];
+#pragma unroll
+        for (int t = 0; t < K; ++t) tmem_ld<TC>(tmem + lane_base + kDCol + NT * (t + K * db) + th * TQ + c0, v[t]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < K; ++t) pin<TC>(v[t]);
+        if (c0 + TC == TQ) {                           // D of this unit fully read: the issuers may reuse it
+          tc_fence_before();
+          __syncwarp();
+          if (lane < K) mbar_arrive(&bar_dempty[lane][db]);
+        }
+        if (DEBUG) {
+          if (r < rows)
+#pragma unroll
+            for (int t = 0; t < K; ++t)
+#pragma unroll
+              for (int i = 0; i < TC; ++i) {
+                const int tok = th * TQ + c0 + i;
+                if (tok < p.ntok) p.Tdbg[(((size_t)(rb * 128 + r) * NG + g) * K + t) * p.ntok + tok] = (int32_t)v[t][i];
+              }
+        } else {
+          float acc[TC];
+#pragma unroll
+          for (int t = 0; t < K; ++t) {
+            const float c = s_c[((k % kRing) * K + t) * 128 + r];
+#pragma unroll
+            for (int i = 0; i < TC; ++i)
+              acc[i] = t == 0 ? c * __int2float_rn((int)v[t][i]) : fmaf(c, __int2float_rn((int)v[t][i]), acc[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < TC; ++i) y[c0 + i] = fmaf(s_sx[k % kRing][th * TQ + c0 + i], acc[i], y[c0 + i]);
+        }
+      }
+      PH(5);
+      g = g + 1 == NG ? 0 : g + 1;
+      if (g == 0) ++rb;
     }
-    if (n > 0) {
-      epilogue(n - 1, kp_g, kp_rb, kp_rows);
-      flush(rb_cur, rows_cur);
-    }
+    PH(6);
+    if (n > 0) flush(rb_cur, rows_of(rb_cur));
     PH(7);
-    if (warp == 0) PH_DUMP(0);
+    if (ew == 0) PH_DUMP(8);
   }
 
   tc_fence_before();
@@ -459,12 +467,12 @@ static Plan make_plan(const sbvr_weights* w) {
   return pl;
 }
 
-static int nt_for(int ntok) { return ntok <= 8 ? 8 : ntok <= 16 ? 16 : ntok <= 32 ? 32 : 64; }
+static int nt_for(int ntok) { return ntok <= 8 ? 8 : ntok <= 16 ? 16 : 32; }
 static size_t cnt_bytes(const Plan& pl) { return ((size_t)(pl.n_rb + 1) * 4 + 255) / 256 * 256; }
 
 template <int K, int NT, bool DEBUG>
 static cudaError_t launch_one(const ZtParams& p, int C, cudaStream_t st) {
-  const int smem = kSlots * ((128 * (16 * K + 5) + 127) / 128 * 128) + 2 * 4 * NT * 32;
+  const int smem = kSlots * ((128 * (16 * K + 5) + 127) / 128 * 128) + 2 * 4 * NT * 32 + kRing * K * 128 * 4;
   static bool attr[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -492,15 +500,13 @@ static cudaError_t launch_k(const ZtParams& p, int C, int NT, bool debug, cudaSt
     switch (NT) {
       case 8: return launch_one<K, 8, true>(p, C, st);
       case 16: return launch_one<K, 16, true>(p, C, st);
-      case 32: return launch_one<K, 32, true>(p, C, st);
-      default: return launch_one<K, 64, true>(p, C, st);
+      default: return launch_one<K, 32, true>(p, C, st);
     }
   }
   switch (NT) {
     case 8: return launch_one<K, 8, false>(p, C, st);
     case 16: return launch_one<K, 16, false>(p, C, st);
-    case 32: return launch_one<K, 32, false>(p, C, st);
-    default: return launch_one<K, 64, false>(p, C, st);
+    default: return launch_one<K, 32, false>(p, C, st);
   }
 }
 

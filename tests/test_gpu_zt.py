@@ -37,8 +37,8 @@ def _enc(pc, s16, b16, ri, K):
 
 
 @pytest.mark.parametrize("M,N,K,T,l", [(128, 128, 4, 1, 8), (144, 256, 4, 8, 8), (256, 512, 3, 13, 8),
-                                       (80, 384, 2, 16, 5), (400, 640, 4, 33, 8), (48, 256, 1, 64, 2),
-                                       (1024, 1024, 4, 40, 8)])
+                                       (80, 384, 2, 16, 5), (400, 640, 4, 32, 8), (48, 256, 1, 31, 2),
+                                       (1024, 1024, 4, 29, 8)])
 def test_zt_sums_bitexact(M, N, K, T, l):
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=M + N + K + T)
     w = sb.pack_canonical(pc, s16, b16, ri, 16)
@@ -71,7 +71,7 @@ def test_zt_gemv_matches_oracle(M, N, K, T):
     assert torch.all(ws.buf == 0xFF)                 # workspace back at rest (counters, slots)
     enc = _enc(pc, s16, b16, ri, K)
     Yh = Y.cpu().numpy()
-    for t in sorted(set([0, T - 1, T // 2, min(T - 1, 63), min(T - 1, 64)])):
+    for t in sorted(set([0, T - 1, T // 2, min(T - 1, 31), min(T - 1, 32)])):
         z, xp, sc = oracle.encode_vector(X[t], 128, 8)
         _close(Yh[t], oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc)))
 

@@ -33,10 +33,12 @@ for _ in range(3):
     torch.cuda.synchronize()
 ts = buf.view(148, 32).cpu().numpy().astype(np.float64)
 units = (a.M // 128) * (a.N // 128) / 148
-names_w = ["B_build", "wait_weights", "expand", "st_wait_arrive", "epi_wait_D", "epi_tmem_ld", "epi_math", "flush"]
+names_e = ["wait_mma(k-2)", "B_build+load_x", "wait_weights", "expand+coef", "st_wait_arrive", "-", "-", "-"]
+names_p = ["-", "-", "-", "-", "wait_D", "ld+math", "loop", "flush"]
 names_i = ["wait_AB", "wait_D_free", "issue_commit"]
 out = {"T": a.T, "units_per_cta": round(units, 2)}
-out["worker_cycles_per_unit"] = {n: round(float(np.median(ts[:, i])) / units, 1) for i, n in enumerate(names_w)}
+out["expand_warp_cycles_per_unit"] = {n: round(float(np.median(ts[:, i])) / units, 1) for i, n in enumerate(names_e) if n != "-"}
+out["epilogue_warp_cycles_per_unit"] = {n: round(float(np.median(ts[:, 8 + i])) / units, 1) for i, n in enumerate(names_p) if n != "-"}
 out["issuer_cycles_per_unit"] = {n: round(float(np.median(ts[:, 16 + i])) / units, 1) for i, n in enumerate(names_i)}
-out["worker_total_per_unit"] = round(float(np.median(ts[:, :8].sum(1))) / units, 1)
+out["expand_total_per_unit"] = round(float(np.median(ts[:, :8].sum(1))) / units, 1)
 print(json.dumps(out))
