@@ -62,6 +62,9 @@ inline int cur_device() {
 #endif
 constexpr int kImmaWarps = SBVR_MMA_WARPS;   // warps per CTA (one CTA per SM: the register file is full)
 constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at least this many units per CTA
+#ifndef SBVR_MMA_OWNER_PULL
+#define SBVR_MMA_OWNER_PULL 0
+#endif
 #ifndef SBVR_MMA_SLOTS
 #define SBVR_MMA_SLOTS 2
 #endif
@@ -731,6 +734,65 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
               if (row < 16 * NB && tk < p.ntok) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
             }
         } else {
+#if SBVR_MMA_OWNER_PULL
+          // owner-pull combine (needs every CTA of the grid co-resident: launched cooperatively)
+          if (b == bA && V0 > b * NG) {
+            // publisher: band b started in an earlier CTA, whose owner pulls this partial.  Plain
+            // stores: every word is self-validating (the slot holds the sentinel until written)
+            float* part = p.ws_part + (size_t)cta * 2 * (TT * 64);
+#pragma unroll
+            for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) __stcg(part + tk * 64 + lane + 32 * h, v[tk][h]);
+          } else {
+            // owner (we hold the band's first unit): pull the later contributors' partials, sum in
+            // CTA order, write y, re-arm their slots for the next launch
+            const int clast = unit_owner(min((b + 1) * NG, p.Us) - 1, p.qq, p.rr);
+            TSW(7);
+            for (int cb = cta + 1; cb <= clast; cb += kSumBatch) {
+              uint32_t vals[kSumBatch][TT][2];
+              // reload the whole batch until no word is the sentinel (a publisher has not written yet):
+              // one L2 round trip per poll, not one per stale word
+              for (long spins = 0;; ++spins) {
+                bool miss = false;
+#pragma unroll
+                for (int j = 0; j < kSumBatch; ++j)
+#pragma unroll
+                  for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                      vals[j][tk][h] = cb + j <= clast
+                                           ? ld_relaxed(p.ws_part + (size_t)(cb + j) * 2 * (TT * 64) + tk * 64 + lane + 32 * h)
+                                           : 0u;
+                      miss |= vals[j][tk][h] == kSentinel;
+                    }
+                if (!__any_sync(0xffffffffu, miss)) break;
+                if (spins > (1L << 24)) __trap();               // a publisher never arrived: fail loudly
+              }
+#pragma unroll
+              for (int j = 0; j < kSumBatch; ++j) {
+                if (cb + j > clast) break;
+#pragma unroll
+                for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+                  for (int h = 0; h < 2; ++h) v[tk][h] += __uint_as_float(vals[j][tk][h]);
+              }
+            }
+            for (int c2 = cta + 1; c2 <= clast; ++c2)
+#pragma unroll
+              for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  reinterpret_cast<unsigned int*>(p.ws_part)[(size_t)c2 * 2 * (TT * 64) + tk * 64 + lane + 32 * h] = kSentinel;
+#pragma unroll
+            for (int tk = 0; tk < TT; ++tk)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int row = lane + 32 * h;
+                if (row < 16 * NB && tk < p.ntok) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
+              }
+          }
+#else
           // band b is shared with other CTAs: last-arriver reduction (no CTA ever waits for another, so
           // nothing depends on the grid being co-resident).  Every contributor stores its CTA partial
           // in its own slot (first / last band of the CTA), fences, and counts itself in on the band's
@@ -805,6 +867,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
                 if (row < 16 * NB && tk < p.ntok) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = sum[tk][h];
               }
           }
+#endif
         }
       }
     }
@@ -840,11 +903,14 @@ inline cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
   cfg.blockDim = dim3(kImmaWarps * 32);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr_pdl[1];
+  cudaLaunchAttribute attr_pdl[2];
   attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  static const int coop = getenv("SBVR_MMA_COOP") ? atoi(getenv("SBVR_MMA_COOP")) : SBVR_MMA_OWNER_PULL;
+  attr_pdl[1].id = cudaLaunchAttributeCooperative;
+  attr_pdl[1].val.cooperative = coop;
   cfg.attrs = attr_pdl;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB>, p);
 }
 
