@@ -30,6 +30,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 import synthetic  # noqa: E402
+from paper_2509_18172_b200 import dist as sdist  # noqa: E402
 
 METRIC = "SBVR GEMV HBM GB/s (% of 8 TB/s) and µs/GEMV at 1/2/4/8 B200 vs fp16 cuBLAS"
 K_BITS, L_BITS, G, N_RATIO = 4, 8, 128, 16
@@ -135,19 +136,13 @@ FUSED = [("qkv_proj", 6144, 4096, 0, ("q_proj", "k_proj", "v_proj")), ("o_proj",
          ("gate_up_proj", 28672, 4096, 2, ("gate_proj", "up_proj")), ("down_proj", 4096, 14336, 3, ("down_proj",))]
 
 
-def shard(M, world, rank):
-    per = M // world
-    assert per % 16 == 0, f"M={M} not divisible into 16-row multiples over {world} ranks"
-    return rank * per, (rank + 1) * per
-
-
 def build_ring(sb, ring, world, rank, device):
     """Ring of `ring` distinct layers of fused matrices; each matrix row-sharded to this rank."""
     layers = []
     for r in range(ring):
         mats = []
         for idx, (name, M, N, xin, _) in enumerate(FUSED):
-            r0, r1 = shard(M, world, rank)
+            r0, r1 = sdist.shard_range(M, world, rank)
             pc, s16, b16, ri = synthetic.random_encoded(r1 - r0, N, K_BITS, N_RATIO, seed=400 + 7 * r + idx + 1000 * rank)
             w = sb.pack_canonical(pc, s16, b16, ri, N_RATIO, device=device)
             mats.append((name, M, N, r0, r1, w, sb.Workspace.for_weights(w, 1), xin))
@@ -189,10 +184,50 @@ def cpu_baseline(budget_s: float = 15.0):
         if time.perf_counter() - t0 > budget_s:
             break
     dt = time.perf_counter() - t0
-    return {"value": done_bytes / dt / 1e9, "unit": "GB/s", "cores": oracle.max_threads(), "kind": "oracle",
+    c1 = oracle_c1_timing()
+    return {"c1": c1, "value": done_bytes / dt / 1e9, "unit": "GB/s", "cores": oracle.max_threads(), "kind": "oracle",
             "sample": f"Llama-3-8B layer set, every {stride}th output row of each of the 7 projections "
                       f"(decode-then-dot fp64 O-Y + O-X activation conversion), {passes} passes in {dt:.1f}s",
             "seconds": dt}
+
+
+def oracle_c1_timing():
+    """SURVEY §8d.7 / BASELINE configs[0] (C1: 1024x1024 fp32 N(0,1), K=4, G=128, one x): the oracle's encode
+    and GEMV wall time on all host cores and on one core.  Encode is timed on a bounded sample of rows (Algorithm
+    1 costs ~tens of ms per group per core) and extrapolated to the 8192 groups of C1 (stated); the GEMV runs
+    the full matrix."""
+    import oracle
+    W = synthetic.gaussian_weight(1024, 1024, seed=0, sigma=1.0)
+    x = synthetic.activation(1024, seed=1)[0]
+    cfg = oracle.OracleConfig(K=K_BITS)
+    cores = oracle.max_threads()
+    out = {"cores": cores, "cpu": _cpu_model(), "groups_total": 8192}
+    for label, nth, rows in (("all_cores", cores, max(1, min(64, cores * 2))), ("1_core", 1, 1)):
+        t0 = time.perf_counter()
+        enc = oracle.encode_matrix(W[:rows], cfg, nthreads=nth)     # also sets the oracle's thread count
+        dt = time.perf_counter() - t0
+        gps = rows * 8 / dt
+        z, xp, sc = oracle.encode_vector(x, G, L_BITS)
+        full = oracle.Encoded(1024, 1024, cfg, np.tile(enc.planes[:1], (1024, 1, 1, 1)), np.tile(enc.s16[:1], (1024, 1)),
+                              np.tile(enc.b16[:1], (1024, 1)), np.tile(enc.r_idx[:1], (1024, 1)), None)
+        t1 = time.perf_counter()
+        oracle.gemv_rows(full, oracle.x_dec_sbvr(z, sc))
+        gdt = time.perf_counter() - t1
+        out[label] = {"threads": nth, "encode_sample_groups": rows * 8, "encode_s_sample": round(dt, 3),
+                      "encode_groups_per_s": round(gps, 2), "c1_encode_s_extrapolated": round(8192 / gps, 1),
+                      "c1_gemv_s": round(gdt, 4)}
+    oracle.encode_matrix(W[:1], cfg, nthreads=cores)               # restore the thread count
+    return out
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 # ------------------------------------------------------------------ main SBVR arm
@@ -219,6 +254,10 @@ def run_sbvr(args, world, rank, local_rank, pg):
         ys = [[torch.zeros(r1 - r0, dtype=torch.float32, device=device) for (_, M, N, r0, r1, w, ws, xin) in mats]
               for mats in layers]
         yfull = [torch.zeros(M, dtype=torch.float32, device=device) for (_, M, N, _, _) in FUSED]
+        symm = None
+        if args.allgather == "symm":                   # (at N = 1 too: exercises the same code path)
+            symm = [[sdist.SymmRowShardedGemv(w, M, 1, pg, ws) for (_, M, N, r0, r1, w, ws, xin) in mats]
+                    for mats in layers]
         y_host = [torch.zeros(M, dtype=torch.float32).pin_memory() for (_, M, N, _, _) in FUSED]
     torch.cuda.synchronize()
 
@@ -232,16 +271,19 @@ def run_sbvr(args, world, rank, local_rank, pg):
         for j, (name, M, N, r0, r1, w, ws, xin) in enumerate(layers[r]):
             if events is not None:
                 cr.record_external(events[j][0], stream)
-            sb.gemv(w, acts[xin], y=ys[r][j], ws=ws)
+            if symm is not None:                        # all-gather fused into the GEMV epilogue (dist.py)
+                symm[r][j](acts[xin])
+            else:
+                sb.gemv(w, acts[xin], y=ys[r][j], ws=ws)
             if events is not None:
                 cr.record_external(events[j][1], stream)
-            if world > 1:
-                torch.distributed.all_gather_into_tensor(yfull[j], ys[r][j], group=pg)
+            if world > 1 and symm is None:
+                sdist.all_gather_rows_into(yfull[j], ys[r][j], group=pg)
         if span is not None:
             cr.record_external(span[1], stream)
         if e2e:
             for j in range(len(layers[r])):
-                src = yfull[j] if world > 1 else ys[r][j]
+                src = symm[r][j].y_full[0] if symm is not None else (yfull[j] if world > 1 else ys[r][j])
                 y_host[j].copy_(src, non_blocking=True)
 
     # --- capture graphs: one plain step graph per ring layer; span-instrumented copies (one event
@@ -426,111 +468,113 @@ def cublas_fp16_baseline(args, device, ring=2, steps=200):
             "how": "torch.matmul fp16 [M,N]x[N] (cuBLAS GEMV) on the same 4 fused matrices, CUDA graph, ring of 2 layers"}
 
 
-def standalone_per_projection(device, iters=100):
-    """us/GEMV of each Llama-3-8B projection alone: CUDA graph of back-to-back sbvr_gemv launches over
-    a ring of distinct weight copies (> 2x L2), device time by CUDA events."""
-    import paper_2509_18172_b200 as sb
-    out = []
+def _graph_stats(stream, launch, iters, replays=15):
+    """Capture `iters` back-to-back launches (launch(i)) in one CUDA graph on `stream`, replay it `replays`
+    times with CUDA events around each replay (on that stream), return per-launch microseconds:
+    (median, p10, p90) over the replays."""
+    with torch.cuda.stream(stream):
+        for i in range(3):
+            launch(i)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(iters):
+                launch(i)
+        g.replay()
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(replays + 1)]
+        evs[0].record(stream)
+        for r in range(replays):
+            g.replay()
+            evs[r + 1].record(stream)
+        torch.cuda.synchronize()
+    us = np.array([evs[r].elapsed_time(evs[r + 1]) * 1e3 / iters for r in range(replays)])
+    return float(np.median(us)), float(np.percentile(us, 10)), float(np.percentile(us, 90))
+
+
+def _ring_count(nbytes):
+    return max(2, int(2.2 * 132e6 // max(nbytes, 1)) + 1)     # distinct copies: ring > 2.2x the 126 MB L2
+
+
+def _cublas_us(device, M, N, T, iters=40):
+    """fp16 dense GEMV / skinny GEMM on the same shape (torch.matmul -> cuBLAS), same ring/graph method."""
     stream = torch.cuda.Stream(device)
-    for name, M, N in layer_shapes():
-        pc, s16, b16, ri = synthetic.random_encoded(M, N, K_BITS, N_RATIO, seed=700 + M + N)
-        w0 = sb.pack_canonical(pc, s16, b16, ri, N_RATIO, device=device)
-        ring = max(2, int(2.2 * 132e6 // w0.nbytes) + 1)
-        ws_ = [w0] + [sb.SbvrWeights(M, N, K_BITS, N_RATIO, w0.data.clone(), w0.ratio_pow.clone()) for _ in range(ring - 1)]
-        wsp = [sb.Workspace.for_weights(w, 1) for w in ws_]
-        act = sb.encode_vector(torch.from_numpy(synthetic.activation(N, seed=6)).to(device))
-        y = torch.empty(M, dtype=torch.float32, device=device)
-        with torch.cuda.stream(stream):
-            for i in range(3):
-                sb.gemv(ws_[i % ring], act, y=y, ws=wsp[i % ring])
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for i in range(iters):
-                    sb.gemv(ws_[i % ring], act, y=y, ws=wsp[i % ring])
-            g.replay()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            g.replay()
-            b.record(stream)
-            torch.cuda.synchronize()
-        us = a.elapsed_time(b) * 1e3 / iters
-        byts = sb.algorithmic_bytes(M, N, K_BITS, act="sbvr", l=L_BITS)
-        out.append({"proj": name, "M": M, "N": N, "us": round(us, 3), "GBps": round(byts / (us * 1e-6) / 1e9, 1),
-                    "ring": ring})
-        del ws_, wsp
-        torch.cuda.empty_cache()
-    return out
+    g = torch.Generator(device="cpu").manual_seed(M + N)
+    W0 = (torch.randn(M, N, generator=g) * 0.02).to(torch.float16).to(device)
+    ring = _ring_count(2 * M * N)
+    Ws = [W0] + [W0.clone() for _ in range(ring - 1)]
+    x = torch.randn(N, T, dtype=torch.float16, device=device) if T > 1 else torch.randn(N, dtype=torch.float16, device=device)
+    out = torch.empty((M, T) if T > 1 else (M,), dtype=torch.float16, device=device)
+    med, p10, p90 = _graph_stats(stream, lambda i: torch.matmul(Ws[i % ring], x, out=out), iters)
+    del Ws, W0
+    torch.cuda.empty_cache()
+    return med
 
 
-def _time_gemv(sb, device, M, N, K, T, act_kind, algo, iters=60, seed=0):
-    """us per GEMV: CUDA graph of back-to-back launches over a ring of distinct weight copies
-    (> 2.2x L2), device time by CUDA events."""
+def _record(sb, device, config, name, M, N, K, T, act_kind, algo, P=1, M_full=None, iters=60, cublas=True, seed=0):
+    """One SURVEY §8d.8 result record: us/GEMV median/p10/p90 over graph replays of `iters` launches on a ring
+    of distinct weight copies (> L2), algorithmic GB/s, fractions of 8 TB/s and of the measured copy peak,
+    cuBLAS fp16 at the same shape and the speedup."""
     pc, s16, b16, ri = synthetic.random_encoded(M, N, K, N_RATIO, seed=seed + M + N + K)
     w0 = sb.pack_canonical(pc, s16, b16, ri, N_RATIO, device=device)
-    ring = max(2, int(2.2 * 132e6 // w0.nbytes) + 1)
+    ring = _ring_count(w0.nbytes)
     ws_ = [w0] + [sb.SbvrWeights(M, N, K, N_RATIO, w0.data.clone(), w0.ratio_pow.clone()) for _ in range(ring - 1)]
     wsp = [sb.Workspace.for_weights(w, T) for w in ws_]
     x = torch.from_numpy(synthetic.activation(N, seed=6, T=T)).to(device)
     act = sb.encode_vector(x) if act_kind == "sbvr" else sb.fp16_activation(x)
     y = torch.empty(T, M, dtype=torch.float32, device=device)
     stream = torch.cuda.Stream(device)
-    with torch.cuda.stream(stream):
-        for i in range(3):
-            sb.gemv_ex(ws_[i % ring], act, y=y, ws=wsp[i % ring], algo=algo)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for i in range(iters):
-                sb.gemv_ex(ws_[i % ring], act, y=y, ws=wsp[i % ring], algo=algo)
-        g.replay()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        g.replay()
-        b.record(stream)
-        torch.cuda.synchronize()
-    us = a.elapsed_time(b) * 1e3 / iters
+    med, p10, p90 = _graph_stats(stream, lambda i: sb.gemv_ex(ws_[i % ring], act, y=y, ws=wsp[i % ring], algo=algo), iters)
     byts = sb.algorithmic_bytes(M, N, K, act=act_kind, l=L_BITS, T=T)
     del ws_, wsp
     torch.cuda.empty_cache()
-    return {"M": M, "N": N, "K": K, "T": T, "x": act_kind, "algo": {0: "auto", 1: "popc", 2: "tc", 3: "mma", 4: "pipe", 5: "zt"}[algo],
-            "us": round(us, 3), "GBps": round(byts / (us * 1e-6) / 1e9, 1)}
+    peak, _ = measured_peak()
+    gbps = byts / (med * 1e-6) / 1e9
+    rec = {"config": config, "shape": name, "M": M, "N": N, "K": K, "l": L_BITS if act_kind == "sbvr" else None,
+           "path": {"sbvr": "SBVR-x", "fp16": "fp16-x"}[act_kind] + "/" + {0: "auto", 1: "popc", 2: "tc", 3: "mma",
+                                                                            4: "pipe", 5: "zt"}[algo],
+           "T": T, "P": P, "bytes_alg": int(byts), "us_median": round(med, 3), "us_p10": round(p10, 3),
+           "us_p90": round(p90, 3), "GBps": round(gbps, 1), "pct_8TBps": round(gbps / 80.0, 2),
+           "pct_measured_peak": round(100 * gbps / peak, 2), "ring": ring}
+    if M_full:
+        rec["M_full"] = M_full
+    if cublas:
+        cu = _cublas_us(device, M, N, T)
+        rec["cublas_us"] = round(cu, 3)
+        rec["speedup_vs_cublas"] = round(cu / med, 3)
+    return rec
+
+
+def records(device):
+    """one record per (config, shape, K, path, T, P) -- C2 Llama-3-8B decode set, C3 Llama-3-70B
+    MLP row shards, C4 Qwen2.5-7B K sweep on both activation paths, C5 batched T = 1..64 -- plus f3."""
+    import paper_2509_18172_b200 as sb
+    out = []
+    for name, M, N in synthetic.LLAMA3_8B_LAYER + [("qkv_fused", 6144, 4096), ("gate_up_fused", 28672, 4096)]:
+        out.append(_record(sb, device, "C2 llama3_8b", name, M, N, K_BITS, 1, "sbvr", sb.ALGO_AUTO, iters=100))
+    for name, M, N in synthetic.LLAMA3_70B_MLP[:2]:
+        for P in (1, 2, 4, 8):
+            out.append(_record(sb, device, "C3 llama3_70b_mlp_row_shard", name, M // P, N, K_BITS, 1, "sbvr",
+                               sb.ALGO_AUTO, P=P, M_full=M, iters=40))
+    for name, M, N in (("q_proj", 3584, 3584), ("k_proj", 512, 3584), ("gate_proj", 18944, 3584), ("down_proj", 3584, 18944)):
+        for K in (2, 3, 4):
+            for kind in ("sbvr", "fp16"):
+                out.append(_record(sb, device, "C4 qwen25_7b", name, M, N, K, 1, kind, sb.ALGO_AUTO,
+                                   cublas=(K == 4 and kind == "sbvr")))
+    for name, M, N in (("q_proj", 4096, 4096), ("gate_proj", 14336, 4096)):
+        for T in (1, 2, 4, 8, 16, 32, 64):
+            out.append(_record(sb, device, "C5 llama3_8b_batched", name, M, N, K_BITS, T, "sbvr", sb.ALGO_AUTO,
+                               iters=40 if T <= 16 else 20))
+            if 2 <= T <= 16:
+                for algo in (sb.ALGO_MMA, sb.ALGO_ZT):
+                    out.append(_record(sb, device, "C5 llama3_8b_batched", name, M, N, K_BITS, T, "sbvr", algo,
+                                       iters=40, cublas=False))
+    return out
 
 
 def sweeps(device):
-    """Configs C4/C5 and the fp16-x path: batched T, K sweep on Qwen-2.5-7B,
-    fp16-x vs SBVR-x.  Diagnostic keys; the headline stays the layer step."""
     import paper_2509_18172_b200 as sb
-    out = {"batched": [], "k_sweep_qwen25_7b": [], "fp16x_llama3_8b": []}
-    for name, M, N in (("q_proj", 4096, 4096), ("gate_proj", 14336, 4096)):
-        for T in (1, 2, 4, 8, 16, 32, 64, 128, 256):
-            for algo in (sb.ALGO_ZT, sb.ALGO_MMA):
-                if algo == sb.ALGO_MMA and T > 16:
-                    continue
-                r = _time_gemv(sb, device, M, N, K_BITS, T, "sbvr", algo, iters=60 if T <= 64 else 20)
-                r["proj"] = name
-                out["batched"].append(r)
-    for name, M, N in (("q_proj", 3584, 3584), ("gate_proj", 18944, 3584), ("down_proj", 3584, 18944)):
-        for K in (2, 3, 4):
-            for kind in ("sbvr", "fp16"):
-                r = _time_gemv(sb, device, M, N, K, 1, kind, sb.ALGO_AUTO)
-                r["proj"] = name
-                out["k_sweep_qwen25_7b"].append(r)
-    for name, M, N in (("q_proj", 4096, 4096), ("gate_proj", 14336, 4096), ("down_proj", 4096, 14336)):
-        for T in (1, 2, 8):
-            r = _time_gemv(sb, device, M, N, K_BITS, T, "fp16", sb.ALGO_AUTO)
-            r["proj"] = name
-            out["fp16x_llama3_8b"].append(r)
-    # config C3 on one GPU: the per-rank row shard of the Llama-3-70B MLP at P = 1, 2, 4, 8 (GEMV-only
-    # scaling; the y all-gather needs P GPUs and is timed by bench.py --gpus P)
-    out["llama3_70b_mlp_row_shards"] = []
-    for name, M, N in synthetic.LLAMA3_70B_MLP:
-        for P in (1, 2, 4, 8):
-            r = _time_gemv(sb, device, M // P, N, K_BITS, 1, "sbvr", sb.ALGO_AUTO, iters=40)
-            r.update(proj=name, P=P, M_full=M)
-            out["llama3_70b_mlp_row_shards"].append(r)
-    out["layer_chain_llama3_8b"] = layer_chain(sb, device)
-    return out
+    return {"records": records(device), "layer_chain_llama3_8b": layer_chain(sb, device)}
 
 
 def layer_chain(sb, device, reps=20):
@@ -633,7 +677,23 @@ def encode_throughput(device):
     torch.cuda.synchronize()
     s = a.elapsed_time(b) / 1e3
     groups = 4096 * 4096 // G
-    out = {"shape": "4096x4096", "seconds": s, "groups_per_s": groups / s, "params_per_s": groups * G / s,
+    # C5 (ii): the whole Llama-3-8B layer set (7 matrices, 218 M params, 1.70 M groups) encoded back to back
+    t_layer, g_layer = 0.0, 0
+    for i, (name, M, N) in enumerate(synthetic.LLAMA3_8B_LAYER):
+        Wl = torch.from_numpy(synthetic.gaussian_weight(M, N, seed=402 + i, sigma=0.02)).to(device)
+        torch.cuda.synchronize()
+        a.record()
+        sb.encode_weights(Wl, K=K_BITS)
+        b.record()
+        torch.cuda.synchronize()
+        t_layer += a.elapsed_time(b) / 1e3
+        g_layer += M * N // G
+        del Wl
+    layer = {"matrices": 7, "groups": g_layer, "params": g_layer * G, "seconds": round(t_layer, 3),
+             "groups_per_s": round(g_layer / t_layer), "params_per_s": round(g_layer * G / t_layer),
+             "full_model_32_layers_s_extrapolated": round(32 * t_layer, 1)}
+    out = {"layer_set_llama3_8b": layer,
+           "shape": "4096x4096", "seconds": s, "groups_per_s": groups / s, "params_per_s": groups * G / s,
            "search_space": "16x64x16 (R x S x B), strict fp64",
            "full_llama3_8b_extrapolated_s": 54525952 / (groups / s)}
     # f2: the encode-time coefficient cache (per-row MRU cache of 8, moving-average admission)
@@ -668,6 +728,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="sbvr", choices=["sbvr", "reference"])
     ap.add_argument("--ring", type=int, default=4)
+    ap.add_argument("--allgather", default="nccl", choices=["nccl", "symm"],
+                    help="N > 1: join y with an NCCL all-gather, or store it to every rank from the GEMV epilogue "
+                         "(symmetric memory, dist.SymmRowShardedGemv)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--no-encode", action="store_true")
@@ -682,19 +745,17 @@ def main():
     if args.impl == "reference":
         return run_reference(args, world, rank)
 
-    if world > 1:
+    if world > 1 or args.allgather == "symm":
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        torch.distributed.init_process_group("nccl", rank=rank, world_size=world,
+                                             device_id=torch.device("cuda", local_rank))
         pg = torch.distributed.group.WORLD
     res, sb = run_sbvr(args, world, rank, local_rank, pg)
     device = torch.device("cuda", local_rank)
     extra = {}
     if rank == 0:
-        if world == 1:
-            try:
-                extra["standalone"] = standalone_per_projection(device)
-            except Exception as e:  # pragma: no cover
-                extra["standalone"] = {"error": str(e)}
         if not args.no_cublas:
             try:
                 extra["cublas"] = cublas_fp16_baseline(args, device)
@@ -774,7 +835,10 @@ def main():
                    "gemvs_per_step": [f"{n} {M}x{N} = {'+'.join(m)}" for n, M, N, _, m in FUSED],
                    "K": K_BITS, "l": L_BITS, "group": G, "batch": 1, "ring_layers": args.ring,
                    "l2": "inputs larger than L2: ring of 4 distinct layer weight sets (468 MB) cycled every step",
-                   "parallelism": f"row-sharded over {world} GPU(s)" + (" + NCCL all-gather of y" if world > 1 else ""),
+                   "parallelism": f"row-sharded over {world} GPU(s)" + ((" + NCCL all-gather of y" if args.allgather == "nccl" else
+                                                                       " + y stored to every rank by the GEMV epilogue "
+                                                                       "(symmetric memory) + signal-pad barrier")
+                                                                      if world > 1 else ""),
                    "path": "sbvr_encode_vector x1 (the 4 layer inputs) + sbvr_gemv x4 (fused qkv, o, fused gate_up, down; "
                            "bit-sliced AND/popcount on the int8 tensor pipe, mma.sync m16n8k32 u8, kernel gemv_mma), "
                            "one CUDA graph per step, programmatic dependent launch"},
@@ -801,8 +865,6 @@ def main():
                   "and event runs under torch.cuda.stream(stream)); value = step algorithmic bytes x K / (last event "
                   "- first event); barrier + synchronize on both sides; max over ranks",
     }
-    if "standalone" in extra:
-        out["us_per_gemv_standalone"] = extra["standalone"]
     if "cublas" in extra:
         cb = extra["cublas"]
         out["vs_cublas_fp16"] = dict(cb)

@@ -183,6 +183,19 @@ sbvr_status sbvr_gemv(const sbvr_weights* w, const sbvr_act* x, float* y, void* 
 sbvr_status sbvr_gemv_batched(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
                               size_t ws_bytes, void* stream);
 
+/* sbvr_gemv_to_peers -- the row-sharded multi-GPU GEMV with the all-gather fused into its epilogue (north star
+ * "row-sharded multi-GPU path ... joins y").  W is this rank's row shard (rows
+ * [y_row_offset, y_row_offset + W.M) of an M_full-row matrix); every y value the kernel produces is stored, over
+ * NVLink, into each of the n_peers (1..8) buffers peer_y[j] -- device pointers, typically the ranks' symmetric-
+ * memory full-y buffers (own rank included), each [T][M_full] fp32 -- at [tau][y_row_offset + row], so no
+ * separate all-gather runs.  peer_y is a HOST array of device pointers.  The caller orders the stores before any
+ * read of the full y on another rank with a signal-pad barrier (dist.py).  Same arithmetic, partition and
+ * determinism as sbvr_gemv_batched on the MMA kernel.  Errors: as sbvr_gemv; SBVR_ERR_SHAPE when the shard does
+ * not fit M_full. */
+sbvr_status sbvr_gemv_to_peers(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* const* peer_y,
+                               int32_t n_peers, int32_t y_row_offset, int32_t M_full, void* workspace, size_t ws_bytes,
+                               void* stream);
+
 /* sbvr_gemv_ex -- as sbvr_gemv_batched with an explicit algorithm (sbvr_algo). */
 sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
                          size_t ws_bytes, int32_t algo, void* stream);

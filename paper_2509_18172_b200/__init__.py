@@ -82,12 +82,17 @@ def lib():
         L.sbvr_fill_ratio_table.argtypes = [P, P]
         L.sbvr_hadamard_rows.argtypes = [P, P, i32, i32, i32, i32, P, P]
         L.sbvr_encode_weights_cached.argtypes = [P, i32, ctypes.c_double, P, i32, i32, i32, P, P, P, P]
-        L.sbvr_debug_zt_sums.argtypes = [P, P, i32, P, P]
+        if hasattr(L, "sbvr_debug_zt_sums"):
+            L.sbvr_debug_zt_sums.argtypes = [P, P, i32, P, P]
+        if hasattr(L, "sbvr_gemv_to_peers"):
+            L.sbvr_gemv_to_peers.argtypes = [P, P, i32, P, i32, i32, i32, P, sz, P]
+        # (A/B timing loads older builds through SBVR_LIB_AB: symbols they lack are simply not declared)
         for name in ("sbvr_weights_bytes", "sbvr_encode_weights", "sbvr_encode_vector", "sbvr_gemv_workspace_bytes",
                      "sbvr_workspace_init", "sbvr_gemv", "sbvr_gemv_batched", "sbvr_gemv_ex", "sbvr_debug_partials",
                      "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows", "sbvr_encode_weights_cached",
-                     "sbvr_debug_zt_sums"):
-            getattr(L, name).restype = i32
+                     "sbvr_debug_zt_sums", "sbvr_gemv_to_peers"):
+            if hasattr(L, name):
+                getattr(L, name).restype = i32
         _lib = L
     return _lib
 
@@ -269,6 +274,18 @@ def gemv_batched(w: SbvrWeights, X: SbvrActivation, Y: Optional[torch.Tensor] = 
     _check(lib().sbvr_gemv_batched(ctypes.byref(wd), ctypes.byref(xd), X.T, _ptr(Y), _ptr(ws.buf), ws.nbytes,
                                    _stream()), "sbvr_gemv_batched")
     return Y
+
+
+def gemv_to_peers(w: SbvrWeights, x: SbvrActivation, peer_ptrs, y_row_offset: int, M_full: int,
+                  ws: Optional[Workspace] = None) -> None:
+    """sbvr_gemv_to_peers: this rank's row-shard GEMV whose epilogue stores y into every peer's full-y buffer
+    (device pointers `peer_ptrs`, [T][M_full] fp32 each) at rows [y_row_offset, y_row_offset + w.M)."""
+    if ws is None:
+        ws = Workspace.for_weights(w, x.T)
+    arr = (ctypes.c_void_p * len(peer_ptrs))(*[int(q) for q in peer_ptrs])
+    wd, xd = w.desc(), x.desc()
+    _check(lib().sbvr_gemv_to_peers(ctypes.byref(wd), ctypes.byref(xd), x.T, arr, len(peer_ptrs), int(y_row_offset),
+                                    int(M_full), _ptr(ws.buf), ws.nbytes, _stream()), "sbvr_gemv_to_peers")
 
 
 def debug_partials(w: SbvrWeights, x: SbvrActivation, algo: int = ALGO_TC) -> torch.Tensor:

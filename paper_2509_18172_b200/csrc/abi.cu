@@ -226,6 +226,31 @@ sbvr_status sbvr_gemv(const sbvr_weights* w, const sbvr_act* x, float* y, void* 
   return sbvr_gemv_ex(w, x, 1, y, workspace, ws_bytes, SBVR_ALGO_AUTO, stream);
 }
 
+sbvr_status sbvr_gemv_to_peers(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* const* peer_y,
+                               int32_t n_peers, int32_t y_row_offset, int32_t M_full, void* workspace, size_t ws_bytes,
+                               void* stream) {
+  sbvr_status s = check_weights(w);
+  if (s != SBVR_OK) return s;
+  s = check_act(w, X, T);
+  if (s != SBVR_OK) return s;
+  if (!peer_y) return set_error(SBVR_ERR_INVALID_ARG, "peer_y is NULL");
+  if (n_peers < 1 || n_peers > 8) return set_error(SBVR_ERR_INVALID_ARG, "n_peers=%d outside 1..8", n_peers);
+  if (y_row_offset < 0 || M_full < w->M || y_row_offset > M_full - w->M)
+    return set_error(SBVR_ERR_SHAPE, "rows [%d, %d) do not fit M_full=%d", y_row_offset, y_row_offset + w->M, M_full);
+  PeerOut po;
+  po.n = n_peers;
+  po.row_offset = y_row_offset;
+  po.M_full = M_full;
+  for (int j = 0; j < 8; ++j) {
+    po.y[j] = j < n_peers ? peer_y[j] : nullptr;
+    if (j < n_peers && !po.y[j]) return set_error(SBVR_ERR_INVALID_ARG, "peer_y[%d] is NULL", j);
+  }
+  size_t need = mma_workspace_bytes(w, T);
+  if (need && (!workspace || ws_bytes < need))
+    return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+  return launch_gemv_mma(w, X, T, nullptr, workspace, ws_bytes, nullptr, (cudaStream_t)stream, &po);
+}
+
 sbvr_status sbvr_gemv_batched(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
                               size_t ws_bytes, void* stream) {
   return sbvr_gemv_ex(w, X, T, Y, workspace, ws_bytes, SBVR_ALGO_AUTO, stream);

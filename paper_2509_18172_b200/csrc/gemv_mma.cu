@@ -89,9 +89,13 @@ static cudaError_t launch_any(int K, const ImmaParams& p, int NB, int TT, bool d
 size_t mma_workspace_bytes(const sbvr_weights* w, int T) { return mma_workspace_bytes_(w, T); }
 
 sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
-                            int32_t* P_debug, cudaStream_t st) {
+                            int32_t* P_debug, cudaStream_t st, const PeerOut* peers) {
   const Plan pl = make_plan(w);
   ImmaParams p;
+  p.n_peers = peers ? peers->n : 0;
+  p.y_off = peers ? peers->row_offset : 0;
+  p.M_full = peers ? peers->M_full : w->M;
+  for (int j = 0; j < 8; ++j) p.peer_y[j] = peers && j < peers->n ? peers->y[j] : nullptr;
   p.ratio_pow = w->ratio_pow;
   p.units = w->data;
   p.K = w->K;
@@ -131,6 +135,7 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
     p.xscales = f16x ? nullptr : x->scales + (size_t)done * pl.NG;
     p.xh = f16x ? xh + (size_t)done * w->N : nullptr;
     p.Y = Y ? Y + (size_t)done * w->M : nullptr;
+    for (int j = 0; j < p.n_peers; ++j) p.peer_y[j] = peers->y[j] + (size_t)done * p.M_full;
     for (int part = 0; part < 2; ++part) {
       const int NB = part == 0 ? 4 : pl.tail_nb;
       const int Us = part == 0 ? pl.Us_main : pl.Us_tail;

@@ -81,7 +81,9 @@ struct ImmaParams {
   const uint16_t* xh;       // [T][N] fp16 x (fp16-x path)
   int ntok;                 // fp16-x: tokens in this pass (<= 8, one per MMA column)
   const float* xscales;     // [T][NG]
-  float* Y;                 // [T][M]
+  float* Y;                 // [T][M] (when n_peers == 0)
+  float* peer_y[8];         // fused row-shard all-gather: y goes to every rank's full-y buffer [T][M_full] at row
+  int n_peers, y_off, M_full;   // offset y_off (symmetric-memory peer pointers; dist.py)
   int32_t* P;               // debug partials [M][NG][K][l]
   float* ws_part;           // [CTA][2][TT][64] partials of a CTA's first / last band when other CTAs share it
                             // (kSentinel words at rest: sbvr_workspace_init, re-armed by the band's reducer)
@@ -207,6 +209,16 @@ __device__ __forceinline__ uint32_t ld_relaxed(const float* ptr) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
   return v;
+}
+
+// y store: local Y, or (fused all-gather epilogue) the same value into every rank's full y over NVLink
+__device__ __forceinline__ void store_y(const ImmaParams& p, int tk, int row, float v) {
+  if (p.n_peers == 0) {
+    p.Y[(size_t)tk * p.M + row] = v;
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < p.n_peers; ++j) p.peer_y[j][(size_t)tk * p.M_full + p.y_off + row] = v;
+  }
 }
 
 __device__ __forceinline__ int unit_owner(int v, int qq, int rr) {
@@ -731,7 +743,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int row = lane + 32 * h;
-              if (row < 16 * NB && tk < p.ntok) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
+              if (row < 16 * NB && tk < p.ntok) store_y(p, tk, 64 * (p.band0 + b) + row, v[tk][h]);
             }
         } else {
 #if SBVR_MMA_OWNER_PULL
@@ -789,7 +801,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int row = lane + 32 * h;
-                if (row < 16 * NB && tk < p.ntok) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = v[tk][h];
+                if (row < 16 * NB && tk < p.ntok) store_y(p, tk, 64 * (p.band0 + b) + row, v[tk][h]);
               }
           }
 #else
@@ -864,7 +876,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int row = lane + 32 * h;
-                if (row < 16 * NB && tk < p.ntok) p.Y[(size_t)tk * p.M + (size_t)64 * (p.band0 + b) + row] = sum[tk][h];
+                if (row < 16 * NB && tk < p.ntok) store_y(p, tk, 64 * (p.band0 + b) + row, sum[tk][h]);
               }
           }
 #endif

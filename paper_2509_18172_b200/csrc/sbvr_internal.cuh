@@ -77,8 +77,13 @@ sbvr_status launch_gemv_fp16x(const sbvr_weights* w, const sbvr_act* x, int T, f
 sbvr_status launch_gemv_tc(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
                            int32_t* P_debug, cudaStream_t st);
 size_t tc_workspace_bytes(const sbvr_weights* w, int T);
+// fused row-shard all-gather epilogue: every y value also lands in each rank's full-y buffer (dist.py)
+struct PeerOut {
+  float* y[8];          // device pointers (symmetric memory; own rank included), each [T][M_full] fp32
+  int n, row_offset, M_full;
+};
 sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
-                            int32_t* P_debug, cudaStream_t st);
+                            int32_t* P_debug, cudaStream_t st, const PeerOut* peers = nullptr);
 size_t mma_workspace_bytes(const sbvr_weights* w, int T);
 sbvr_status launch_gemv_pipe(const sbvr_weights* w, const sbvr_act* x, float* y, void* ws, int32_t* P_debug,
                              cudaStream_t st);

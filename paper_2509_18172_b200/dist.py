@@ -5,7 +5,14 @@ group: rank p owns rows [p*M/P, (p+1)*M/P) of every matrix, encodes and stores o
 runs sbvr_gemv on it, and the full y is joined with one all-gather.  On GPUs the process group
 is NCCL (NVLink 5 / NVSwitch); the same host logic runs under gloo in the CPU tests.
 
-Nothing here touches the C-ABI directly; the per-rank compute is the library's sbvr_gemv.
+Two ways to join y:
+- `RowShardedGemv` (+ `sbvr_row_sharded`): the local GEMV, then an NCCL all-gather of the y shards;
+- `SymmRowShardedGemv`: the all-gather fused into the GEMV's epilogue -- every rank's kernel stores its y rows
+  directly into every rank's full-y buffer in symmetric memory (torch.distributed._symmetric_memory: the same
+  allocation mapped on all GPUs of the node, reached over NVLink 5 / NVSwitch), then one signal-pad barrier
+  orders those stores before y is read (sbvr_gemv_to_peers; no NCCL call on the data path).
+
+The per-rank compute is always the library's CUDA GEMV through the C-ABI.
 """
 from __future__ import annotations
 
@@ -39,6 +46,11 @@ def gather_rows(y_local: torch.Tensor, group=None) -> torch.Tensor:
     return torch.cat(parts, dim=-1)
 
 
+def all_gather_rows_into(out: torch.Tensor, y_local: torch.Tensor, group=None) -> None:
+    """NCCL all-gather of 1-D y shards into a preallocated full y (capturable; bench.py's N > 1 step)."""
+    dist.all_gather_into_tensor(out, y_local, group=group)
+
+
 class RowShardedGemv:
     """y = W x with W row-sharded across the process group.
 
@@ -56,6 +68,41 @@ class RowShardedGemv:
     def __call__(self, x) -> torch.Tensor:
         y_local = self.local_gemv(self.r0, self.r1, x)
         return gather_rows(y_local, self.group) if self.world > 1 else y_local
+
+
+def peer_row_offsets(M: int, world: int):
+    """Row offset of every rank's shard in the full y (what each rank's fused epilogue writes to)."""
+    return [shard_range(M, world, r)[0] for r in range(world)]
+
+
+class SymmRowShardedGemv:
+    """y = W x, W row-sharded over the group, the all-gather fused into the GEMV epilogue.
+
+    A symmetric-memory buffer y_full [T][M] exists on every rank; rank p's sbvr_gemv_to_peers launch stores rows
+    [r0, r1) of y into all ranks' y_full through their peer pointers, then `barrier()` (signal pads, device
+    side) makes every rank's stores visible before anyone reads y_full.  Capturable in a CUDA graph."""
+
+    def __init__(self, w_shard, M: int, T: int = 1, group=None, ws: Optional[object] = None):
+        import paper_2509_18172_b200 as sb
+        import torch.distributed._symmetric_memory as symm_mem
+        self.sb = sb
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.M, self.T = M, T
+        self.r0, self.r1 = shard_range(M, self.world, self.rank)
+        assert w_shard.M == self.r1 - self.r0
+        self.w = w_shard
+        self.ws = ws if ws is not None else sb.Workspace.for_weights(w_shard, T)
+        self.y_full = symm_mem.empty((T, M), dtype=torch.float32, device=w_shard.data.device)
+        self.hdl = symm_mem.rendezvous(self.y_full, self.group)
+        self.peer_ptrs = [int(p) for p in self.hdl.buffer_ptrs]
+        assert len(self.peer_ptrs) == self.world
+
+    def __call__(self, act) -> torch.Tensor:
+        self.sb.gemv_to_peers(self.w, act, self.peer_ptrs, self.r0, self.M, self.ws)
+        self.hdl.barrier(channel=0)
+        return self.y_full if self.T > 1 else self.y_full[0]
 
 
 def encode_shard(W_full: torch.Tensor, world: int, rank: int, **kw):

@@ -78,3 +78,45 @@ def test_shard_ranges_cover_rows():
             assert all((r1 - r0) % 16 == 0 for r0, r1 in rs)
     with pytest.raises(ValueError):
         shard_range(1000, 8, 0)
+
+
+def _peer_worker(rank, world, port, shared, q):
+    """Emulates the fused epilogue on CPU: every rank writes its shard's y (oracle) into ONE shared full-y
+    buffer at its peer_row_offsets entry -- the addressing sbvr_gemv_to_peers uses on every peer."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import synthetic
+        from paper_2509_18172_b200.dist import peer_row_offsets, shard_range
+        M, N, K = 96, 256, 4
+        pc, s16, b16, ri = synthetic.random_encoded(M, N, K, 16, seed=8)
+        x = synthetic.activation(N, seed=9)[0]
+        z, xp, sc = oracle.encode_vector(x, 128, 8)
+        r0, r1 = shard_range(M, world, rank)
+        assert peer_row_offsets(M, world)[rank] == r0
+        enc = oracle.Encoded(r1 - r0, N, oracle.OracleConfig(K=K), pc[r0:r1].copy(), s16[r0:r1].copy(),
+                             b16[r0:r1].copy(), ri[r0:r1].copy(), None)
+        shared[r0:r1] = torch.from_numpy(oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc)))
+        dist.barrier()                                   # stands in for the signal-pad barrier
+        full = oracle.gemv_rows(oracle.Encoded(M, N, oracle.OracleConfig(K=K), pc, s16, b16, ri, None),
+                                oracle.x_dec_sbvr(z, sc))
+        q.put((rank, bool(np.array_equal(shared.numpy(), full))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_epilogue_addressing_gloo_world3():
+    world = 3
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    shared = torch.full((96,), float("nan"), dtype=torch.float64).share_memory_()
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, shared, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == [0, 1, 2] and all(r[1] for r in res), res
