@@ -310,3 +310,69 @@ def encode_matrix_cached(W, cfg: OracleConfig, cache_size: int = 8, alpha: float
                                       _p(b16), _p(ri), _p(mse), _p(hit))
     return Encoded(M, N, cfg, planes, s16, b16, ri, mse), hit
 
+
+
+# ------------------------------------------------------------------ coefficient table + per-group index (f2)
+def table_sample_positions(n_groups: int, n_table: int):
+    """Reading A23: the coefficient table is seeded from min(n_table, n_groups) evenly spaced groups,
+    q_i = floor(i * n_groups / n_sample) in row-major (row, group) order."""
+    n_s = min(n_table, n_groups)
+    return [i * n_groups // n_s for i in range(n_s)]
+
+
+@dataclass
+class IndexedEncoded:
+    """SBVR weights in the table + index format: planes as Encoded, a coefficient table of
+    (r_idx, s16, b16) entries and one u8 table index per group."""
+    M: int
+    N: int
+    cfg: OracleConfig
+    planes: np.ndarray   # [M][N/G][K][G/32] uint32
+    idx: np.ndarray      # [M][N/G] uint8
+    table: np.ndarray    # [n][3] (r_idx, s16, b16) as int64
+    mse: np.ndarray      # [M][N/G] float64
+
+    def expand(self) -> Encoded:
+        """The per-group meta the table entries stand for (same decode, the plain format)."""
+        t = self.table[self.idx.astype(np.int64)]
+        return Encoded(self.M, self.N, self.cfg, self.planes, t[..., 1].astype(np.uint16), t[..., 2].astype(np.uint16),
+                       t[..., 0].astype(np.uint8), self.mse)
+
+
+def encode_matrix_indexed(W, cfg: OracleConfig, n_table: int) -> IndexedEncoded:
+    """f2 storage ("a coefficient cache containing all coefficient sets required for decoding, as well as a
+    coefficient index that identifies the specific coefficient set used by each K-bit bitvector set"; P:233 the
+    cache of previously selected r, s, b), reading A23, step by step:
+      1. Algorithm 1 (encode_group) on the table_sample_positions groups;
+      2. the table = their winning (r_idx, s16, b16) triples, duplicates dropped, in sample order (<= n_table <= 256);
+      3. every group takes the table entry of least MSE (entry_mse, strict '<' in table order: the first best) and
+         its bits are assigned for that entry's coefficients."""
+    W = np.ascontiguousarray(np.asarray(W, np.float32))
+    M, N = W.shape
+    G, K = cfg.group_size, cfg.K
+    NG = N // G
+    assert 1 <= n_table <= 256
+    table = []
+    for q in table_sample_positions(M * NG, n_table):
+        r, g = divmod(q, NG)
+        e = encode_group(W[r, g * G:(g + 1) * G].astype(np.float64), cfg)
+        t = (int(e["r_idx"]), int(e["s16"]), int(e["b16"]))
+        if t not in table:
+            table.append(t)
+    R = ratio_set(cfg.n_ratio)
+    planes = np.zeros((M, NG, K, G // 32), np.uint32)
+    idx = np.zeros((M, NG), np.uint8)
+    mse = np.zeros((M, NG), np.float64)
+    for r in range(M):
+        for g in range(NG):
+            X = W[r, g * G:(g + 1) * G].astype(np.float64)
+            best, best_m = 0, None
+            for e, (ri, s16, b16) in enumerate(table):
+                m = entry_mse(X, K, R[ri], fp16_to_double(s16), fp16_to_double(b16))
+                if best_m is None or m < best_m:
+                    best, best_m = e, m
+            ri, s16, b16 = table[best]
+            planes[r, g] = assign(X, coefficients(R[ri], fp16_to_double(s16), fp16_to_double(b16), K))
+            idx[r, g] = best
+            mse[r, g] = best_m
+    return IndexedEncoded(M, N, cfg, planes, idx, np.asarray(table, np.int64).reshape(-1, 3), mse)
