@@ -672,10 +672,22 @@ def encode_throughput(device):
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    sb.encode_weights(W, K=K_BITS)
+    _, m_full_all = sb.encode_weights(W, K=K_BITS, return_mse=True)
     b.record()
     torch.cuda.synchronize()
     s = a.elapsed_time(b) / 1e3
+    # f2 storage (reading A23): coefficient table (256 entries) + a 1-byte index per group
+    a.record()
+    w_idx, m_idx = sb.encode_weights_indexed(W, K=K_BITS, n_table=256)
+    b.record()
+    torch.cuda.synchronize()
+    s_idx = a.elapsed_time(b) / 1e3
+    indexed = {"n_table": 256, "table_entries": int(w_idx.coef_table[0].item()), "seconds": round(s_idx, 3),
+               "groups_per_s": round(4096 * 4096 / G / s_idx), "meta_bytes_per_group": 1.0,
+               "weight_bytes": int(w_idx.data.numel()), "weight_bytes_5B_meta": int(sb.weights_bytes(4096, 4096, K_BITS)[0]),
+               "mean_mse": m_idx.mean().item(), "mean_mse_full_search": m_full_all.mean().item(),
+               "max_mse": m_idx.max().item(), "max_mse_full_search": m_full_all.max().item()}
+    del w_idx, m_idx
     groups = 4096 * 4096 // G
     # C5 (ii): the whole Llama-3-8B layer set (7 matrices, 218 M params, 1.70 M groups) encoded back to back
     t_layer, g_layer = 0.0, 0
@@ -692,7 +704,7 @@ def encode_throughput(device):
     layer = {"matrices": 7, "groups": g_layer, "params": g_layer * G, "seconds": round(t_layer, 3),
              "groups_per_s": round(g_layer / t_layer), "params_per_s": round(g_layer * G / t_layer),
              "full_model_32_layers_s_extrapolated": round(32 * t_layer, 1)}
-    out = {"layer_set_llama3_8b": layer,
+    out = {"layer_set_llama3_8b": layer, "indexed": indexed,
            "shape": "4096x4096", "seconds": s, "groups_per_s": groups / s, "params_per_s": groups * G / s,
            "search_space": "16x64x16 (R x S x B), strict fp64",
            "full_llama3_8b_extrapolated_s": 54525952 / (groups / s)}

@@ -45,6 +45,9 @@
  *   scale/bias word r = fp16 s (bits 0-15) | fp16 b (bits 16-31); ratio-index byte r = uint8
  *   index into R.
  *   ratio_pow [n_ratio][K] fp32 = r_i^t (repeated multiplication in fp64, rounded to fp32).
+ *   SBVR_META_INDEXED: the same records with the 5-byte meta replaced by one byte per row:
+ *       [R x 16K bytes: bit-planes][R x 1 B: coefficient-table index]   (total M*N*K/8 + M*N/128 bytes)
+ *   and the coefficient table in coef_table (2 KB).
  *
  * Device activation layout (SBVR-x, written by sbvr_encode_vector):
  *   planes [T][N/G][l][G/32] uint32 (same bit order as the weights), scales [T][N/G] fp32.
@@ -60,7 +63,7 @@
 extern "C" {
 #endif
 
-#define SBVR_ABI_VERSION 1
+#define SBVR_ABI_VERSION 2
 
 typedef enum {
   SBVR_OK = 0,
@@ -109,11 +112,22 @@ typedef struct {
   int32_t strict;        /* 1 = fp64 search bit-identical to the oracle (only mode in this build) */
 } sbvr_encode_config;
 
-/* Encoded weights (device pointers, caller-owned; sizes from sbvr_weights_bytes). */
+/* Per-group coefficient metadata of a weight buffer. */
+typedef enum {
+  SBVR_META_GROUP = 0,   /* every group stores fp16 s, fp16 b and a u8 ratio index (5 B per group) */
+  SBVR_META_INDEXED = 1  /* every group stores a u8 index into a per-matrix coefficient table (1 B per group):
+                            "a coefficient cache containing all coefficient sets required for decoding, as well
+                            as a coefficient index" */
+} sbvr_meta_kind;
+
+/* Encoded weights (device pointers, caller-owned; sizes from sbvr_weights_bytes / sbvr_weights_bytes_ex). */
 typedef struct {
   int32_t M, N, K, group_size, n_ratio;
   uint8_t* data;         /* packed units (layout above), 16-byte aligned */
   float* ratio_pow;      /* [n_ratio][K], 16-byte aligned */
+  int32_t meta_kind;     /* sbvr_meta_kind; SBVR_META_GROUP unless the weights come from the indexed encoder */
+  uint32_t* coef_table;  /* SBVR_META_INDEXED: [1 + 2 * 256] u32 -- word 0 = number of entries n (1..256), then
+                            per entry (fp16 s | fp16 b << 16, ratio index); NULL for SBVR_META_GROUP */
 } sbvr_weights;
 
 /* One activation descriptor; for T vectors the buffers hold T contiguous vectors. */
@@ -142,6 +156,22 @@ sbvr_status sbvr_weights_bytes(int32_t M, int32_t N, int32_t K, int32_t group_si
  * group's winning MSE.  Groups run in parallel on the GPU. */
 sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, int32_t dtype, int32_t M,
                                 int32_t N, const sbvr_weights* out, double* group_mse, void* stream);
+
+/* Byte sizes for either meta kind (sbvr_weights_bytes = SBVR_META_GROUP); table = bytes of coef_table. */
+sbvr_status sbvr_weights_bytes_ex(int32_t M, int32_t N, int32_t K, int32_t group_size, int32_t n_ratio,
+                                  int32_t meta_kind, size_t* data_bytes, size_t* ratio_pow_bytes, size_t* table_bytes);
+
+/* sbvr_encode_weights_indexed -- SBVR weights in the table + index format (P:233's cache of previously
+ * selected r, s, b; reading A23): (1) Algorithm 1, exactly as sbvr_encode_weights, on min(n_table, groups) evenly
+ * spaced sample groups (row-major group q_i = floor(i * groups / n_sample)); (2) the coefficient table = their
+ * winning (r, s, b), duplicates dropped, in sample order; (3) every group takes the table entry of least MSE
+ * (strict '<' in table order) and its bits are assigned for that entry.  n_table: 1..256.  out must have
+ * meta_kind = SBVR_META_INDEXED, data sized by sbvr_weights_bytes_ex and coef_table set.  group_mse as in
+ * sbvr_encode_weights.  workspace: device scratch of >= 8 * n_table bytes.  Strict fp64, bit-identical with the
+ * oracle; all work on `stream`. */
+sbvr_status sbvr_encode_weights_indexed(const sbvr_encode_config* cfg, int32_t n_table, const void* W, int32_t dtype,
+                                        int32_t M, int32_t N, const sbvr_weights* out, double* group_mse,
+                                        void* workspace, size_t ws_bytes, void* stream);
 
 /* sbvr_encode_weights_cached -- the encode-time coefficient cache of P:233 (§4.2 and its footnote):
  * "we maintain a cache of previously selected variables r, s, and b ... check the cache ... before
@@ -227,6 +257,13 @@ sbvr_status sbvr_pack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_s
                                 const uint16_t* s16, const uint16_t* b16, const uint8_t* r_idx, uint8_t* data);
 sbvr_status sbvr_unpack_canonical(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint8_t* data,
                                   uint32_t* planes_canon, uint16_t* s16, uint16_t* b16, uint8_t* r_idx);
+
+/* Indexed-format host transforms: canonical planes [M][N/G][K][G/32] + table index [M][N/G] u8 <-> the packed
+ * SBVR_META_INDEXED image `data` (size from sbvr_weights_bytes_ex).  Bit-exact inverses. */
+sbvr_status sbvr_pack_indexed(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_canon,
+                              const uint8_t* idx, uint8_t* data);
+sbvr_status sbvr_unpack_indexed(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint8_t* data,
+                                uint32_t* planes_canon, uint8_t* idx);
 
 /* Write w->ratio_pow (device) for w->n_ratio, w->K (used when weights arrive via pack). */
 sbvr_status sbvr_fill_ratio_table(const sbvr_weights* w, void* stream);

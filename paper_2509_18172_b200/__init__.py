@@ -26,6 +26,7 @@ OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_ALIGNMENT, ERR_CUDA, ERR_WO
 F32, F16, BF16 = 0, 1, 2
 ACT_FP16, ACT_SBVR = 0, 1
 ALGO_AUTO, ALGO_POPC, ALGO_TC, ALGO_MMA, ALGO_PIPE, ALGO_ZT = 0, 1, 2, 3, 4, 5
+META_GROUP, META_INDEXED = 0, 1
 G = 128
 
 
@@ -43,7 +44,8 @@ class _EncCfg(ctypes.Structure):
 
 class _Weights(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("N", ctypes.c_int32), ("K", ctypes.c_int32), ("group_size", ctypes.c_int32),
-                ("n_ratio", ctypes.c_int32), ("data", ctypes.c_void_p), ("ratio_pow", ctypes.c_void_p)]
+                ("n_ratio", ctypes.c_int32), ("data", ctypes.c_void_p), ("ratio_pow", ctypes.c_void_p),
+                ("meta_kind", ctypes.c_int32), ("coef_table", ctypes.c_void_p)]
 
 
 class _Act(ctypes.Structure):
@@ -84,13 +86,20 @@ def lib():
         L.sbvr_encode_weights_cached.argtypes = [P, i32, ctypes.c_double, P, i32, i32, i32, P, P, P, P]
         if hasattr(L, "sbvr_debug_zt_sums"):
             L.sbvr_debug_zt_sums.argtypes = [P, P, i32, P, P]
+        for name, at in (("sbvr_weights_bytes_ex", [i32, i32, i32, i32, i32, i32, P, P, P]),
+                         ("sbvr_encode_weights_indexed", [P, i32, P, i32, i32, i32, P, P, P, sz, P]),
+                         ("sbvr_pack_indexed", [i32, i32, i32, i32, P, P, P]),
+                         ("sbvr_unpack_indexed", [i32, i32, i32, i32, P, P, P])):
+            if hasattr(L, name):
+                getattr(L, name).argtypes = at
         if hasattr(L, "sbvr_gemv_to_peers"):
             L.sbvr_gemv_to_peers.argtypes = [P, P, i32, P, i32, i32, i32, P, sz, P]
         # (A/B timing loads older builds through SBVR_LIB_AB: symbols they lack are simply not declared)
         for name in ("sbvr_weights_bytes", "sbvr_encode_weights", "sbvr_encode_vector", "sbvr_gemv_workspace_bytes",
                      "sbvr_workspace_init", "sbvr_gemv", "sbvr_gemv_batched", "sbvr_gemv_ex", "sbvr_debug_partials",
                      "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows", "sbvr_encode_weights_cached",
-                     "sbvr_debug_zt_sums", "sbvr_gemv_to_peers"):
+                     "sbvr_debug_zt_sums", "sbvr_gemv_to_peers", "sbvr_weights_bytes_ex",
+                     "sbvr_encode_weights_indexed", "sbvr_pack_indexed", "sbvr_unpack_indexed"):
             if hasattr(L, name):
                 getattr(L, name).restype = i32
         _lib = L
@@ -125,9 +134,12 @@ class SbvrWeights:
     n_ratio: int
     data: torch.Tensor        # uint8, packed unit records (include/sbvr.h device layout)
     ratio_pow: torch.Tensor   # float32 [n_ratio, K]
+    meta_kind: int = 0        # META_GROUP (5 B per group) or META_INDEXED (1 B index + coef_table)
+    coef_table: Optional[torch.Tensor] = None   # META_INDEXED: int32 [1 + 2*256] (n, then (s16|b16<<16, r_idx))
 
     def desc(self) -> _Weights:
-        return _Weights(self.M, self.N, self.K, G, self.n_ratio, self.data.data_ptr(), self.ratio_pow.data_ptr())
+        return _Weights(self.M, self.N, self.K, G, self.n_ratio, self.data.data_ptr(), self.ratio_pow.data_ptr(),
+                        self.meta_kind, self.coef_table.data_ptr() if self.coef_table is not None else 0)
 
     @property
     def nbytes(self) -> int:
@@ -139,6 +151,77 @@ def weights_bytes(M: int, N: int, K: int, n_ratio: int = 16):
     out = [ctypes.c_size_t() for _ in range(2)]
     _check(lib().sbvr_weights_bytes(M, N, K, G, n_ratio, *[ctypes.byref(o) for o in out]), "sbvr_weights_bytes")
     return tuple(o.value for o in out)
+
+
+def weights_bytes_ex(M: int, N: int, K: int, n_ratio: int = 16, meta_kind: int = META_GROUP):
+    out = [ctypes.c_size_t() for _ in range(3)]
+    _check(lib().sbvr_weights_bytes_ex(M, N, K, G, n_ratio, meta_kind, *[ctypes.byref(o) for o in out]),
+           "sbvr_weights_bytes_ex")
+    return tuple(o.value for o in out)
+
+
+def weights_empty_indexed(M: int, N: int, K: int, n_ratio: int = 16, device="cuda") -> SbvrWeights:
+    db, rpb, tb = weights_bytes_ex(M, N, K, n_ratio, META_INDEXED)
+    dev = torch.device(device)
+    return SbvrWeights(M, N, K, n_ratio, torch.empty(db, dtype=torch.uint8, device=dev),
+                       torch.empty((n_ratio, K), dtype=torch.float32, device=dev), META_INDEXED,
+                       torch.zeros(tb // 4, dtype=torch.int32, device=dev))
+
+
+def encode_weights_indexed(W: torch.Tensor, K: int = 4, n_table: int = 256, n_ratio: int = 16, n_scale: int = 64,
+                           n_bias: int = 16, s_min_factor: float = 2.0, out: Optional[SbvrWeights] = None):
+    """sbvr_encode_weights_indexed (reading A23): coefficient table + a u8 index per group.
+    Returns (weights, group MSE [M, N/G] fp64)."""
+    assert W.is_cuda and W.dim() == 2 and W.is_contiguous()
+    M, N = W.shape
+    w = out if out is not None else weights_empty_indexed(M, N, K, n_ratio, W.device)
+    cfg = _EncCfg(K, G, n_ratio, n_scale, n_bias, float(s_min_factor), 1)
+    mse = torch.empty((M, N // G), dtype=torch.float64, device=W.device)
+    scratch = torch.empty(8 * n_table, dtype=torch.uint8, device=W.device)
+    d = w.desc()
+    _check(lib().sbvr_encode_weights_indexed(ctypes.byref(cfg), int(n_table), _ptr(W), _DT[W.dtype], M, N,
+                                             ctypes.byref(d), _ptr(mse), _ptr(scratch), scratch.numel(), _stream()),
+           "sbvr_encode_weights_indexed")
+    return w, mse
+
+
+def table_entries(w: SbvrWeights) -> np.ndarray:
+    """The coefficient table of indexed weights as [n][3] (r_idx, s16, b16) int64 (host copy)."""
+    t = w.coef_table.cpu().numpy().view(np.uint32)
+    n = int(t[0])
+    e = t[1:1 + 2 * n].reshape(n, 2)
+    return np.stack([e[:, 1], e[:, 0] & 0xFFFF, e[:, 0] >> 16], 1).astype(np.int64)
+
+
+def pack_indexed(planes_canon: np.ndarray, idx: np.ndarray, table: np.ndarray, n_ratio: int = 16,
+                 device="cuda") -> SbvrWeights:
+    """Canonical planes + u8 table index + table [n][3] (r_idx, s16, b16) -> device indexed SbvrWeights."""
+    M, NG, K, _ = planes_canon.shape
+    db, _, tb = weights_bytes_ex(M, NG * G, K, n_ratio, META_INDEXED)
+    data = np.zeros(db, np.uint8)
+    _check(lib().sbvr_pack_indexed(M, NG * G, K, G, _np_ptr(np.ascontiguousarray(planes_canon, np.uint32)),
+                                   _np_ptr(np.ascontiguousarray(idx, np.uint8)), _np_ptr(data)), "sbvr_pack_indexed")
+    tab = np.zeros(tb // 4, np.uint32)
+    table = np.asarray(table, np.int64).reshape(-1, 3)
+    tab[0] = len(table)
+    tab[1:1 + 2 * len(table):2] = (table[:, 1] | (table[:, 2] << 16)).astype(np.uint32)
+    tab[2:2 + 2 * len(table):2] = table[:, 0].astype(np.uint32)
+    w = weights_empty_indexed(M, NG * G, K, n_ratio, device)
+    w.data.copy_(torch.from_numpy(data))
+    w.coef_table.copy_(torch.from_numpy(tab.view(np.int32)))
+    d = w.desc()
+    _check(lib().sbvr_fill_ratio_table(ctypes.byref(d), _stream()), "sbvr_fill_ratio_table")
+    return w
+
+
+def unpack_indexed(w: SbvrWeights):
+    """Device indexed SbvrWeights -> canonical planes [M][N/G][K][4] uint32 and index [M][N/G] uint8."""
+    NG = w.N // G
+    pc = np.zeros((w.M, NG, w.K, 4), np.uint32)
+    idx = np.zeros((w.M, NG), np.uint8)
+    data = np.ascontiguousarray(w.data.cpu().numpy(), np.uint8)
+    _check(lib().sbvr_unpack_indexed(w.M, w.N, w.K, G, _np_ptr(data), _np_ptr(pc), _np_ptr(idx)), "sbvr_unpack_indexed")
+    return pc, idx
 
 
 def weights_empty(M: int, N: int, K: int, n_ratio: int = 16, device="cuda") -> SbvrWeights:

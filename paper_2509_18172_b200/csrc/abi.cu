@@ -42,6 +42,12 @@ static sbvr_status check_weights(const sbvr_weights* w) {
   if (w->N % kG) return set_error(SBVR_ERR_SHAPE, "N=%d not a multiple of group_size 128", w->N);
   if (!aligned16(w->data) || !aligned16(w->ratio_pow))
     return set_error(SBVR_ERR_ALIGNMENT, "weights buffers must be 16-byte aligned");
+  if (w->meta_kind != SBVR_META_GROUP && w->meta_kind != SBVR_META_INDEXED)
+    return set_error(SBVR_ERR_INVALID_ARG, "unknown meta_kind %d", w->meta_kind);
+  if (w->meta_kind == SBVR_META_INDEXED) {
+    if (!w->coef_table) return set_error(SBVR_ERR_INVALID_ARG, "indexed weights need coef_table");
+    if (!aligned16(w->coef_table)) return set_error(SBVR_ERR_ALIGNMENT, "coef_table must be 16-byte aligned");
+  }
   return SBVR_OK;
 }
 
@@ -100,6 +106,22 @@ sbvr_status sbvr_weights_bytes(int32_t M, int32_t N, int32_t K, int32_t group_si
   return SBVR_OK;
 }
 
+sbvr_status sbvr_weights_bytes_ex(int32_t M, int32_t N, int32_t K, int32_t group_size, int32_t n_ratio,
+                                  int32_t meta_kind, size_t* data_bytes, size_t* ratio_pow_bytes, size_t* table_bytes) {
+  if (!table_bytes) return set_error(SBVR_ERR_INVALID_ARG, "output pointer is NULL");
+  sbvr_status s = sbvr_weights_bytes(M, N, K, group_size, n_ratio, data_bytes, ratio_pow_bytes);
+  if (s != SBVR_OK) return s;
+  if (meta_kind == SBVR_META_GROUP) {
+    *table_bytes = 0;
+  } else if (meta_kind == SBVR_META_INDEXED) {
+    *data_bytes = (size_t)IdxLayout(M, N, K).total_bytes();
+    *table_bytes = kTableBytes;
+  } else {
+    return set_error(SBVR_ERR_INVALID_ARG, "unknown meta_kind %d", meta_kind);
+  }
+  return SBVR_OK;
+}
+
 static sbvr_status check_encode(const sbvr_encode_config* cfg, const void* W, int32_t dtype, int32_t M, int32_t N,
                                 const sbvr_weights* out) {
   if (!cfg || !W || !out) return set_error(SBVR_ERR_INVALID_ARG, "cfg/W/out is NULL");
@@ -122,7 +144,21 @@ sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, in
                                 const sbvr_weights* out, double* group_mse, void* stream) {
   sbvr_status s = check_encode(cfg, W, dtype, M, N, out);
   if (s != SBVR_OK) return s;
+  if (out->meta_kind != SBVR_META_GROUP) return set_error(SBVR_ERR_INVALID_ARG, "out must be SBVR_META_GROUP");
   return launch_encode_weights(cfg, W, dtype, M, N, out, group_mse, -1, 0.0, nullptr, (cudaStream_t)stream);
+}
+
+sbvr_status sbvr_encode_weights_indexed(const sbvr_encode_config* cfg, int32_t n_table, const void* W, int32_t dtype,
+                                        int32_t M, int32_t N, const sbvr_weights* out, double* group_mse,
+                                        void* workspace, size_t ws_bytes, void* stream) {
+  sbvr_status s = check_encode(cfg, W, dtype, M, N, out);
+  if (s != SBVR_OK) return s;
+  if (out->meta_kind != SBVR_META_INDEXED) return set_error(SBVR_ERR_INVALID_ARG, "out must be SBVR_META_INDEXED");
+  if (n_table < 1 || n_table > kMaxTable) return set_error(SBVR_ERR_INVALID_ARG, "n_table=%d outside 1..256", n_table);
+  if (!workspace || ws_bytes < (size_t)8 * n_table)
+    return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, (size_t)8 * n_table);
+  return launch_encode_indexed(cfg, n_table, W, dtype, M, N, out, group_mse, static_cast<uint32_t*>(workspace),
+                               (cudaStream_t)stream);
 }
 
 sbvr_status sbvr_encode_weights_cached(const sbvr_encode_config* cfg, int32_t cache_size, double ema_alpha,
@@ -130,6 +166,7 @@ sbvr_status sbvr_encode_weights_cached(const sbvr_encode_config* cfg, int32_t ca
                                        double* group_mse, uint8_t* group_hit, void* stream) {
   sbvr_status s = check_encode(cfg, W, dtype, M, N, out);
   if (s != SBVR_OK) return s;
+  if (out->meta_kind != SBVR_META_GROUP) return set_error(SBVR_ERR_INVALID_ARG, "out must be SBVR_META_GROUP");
   if (cache_size < 0 || cache_size > 64) return set_error(SBVR_ERR_INVALID_ARG, "cache_size=%d outside 0..64", cache_size);
   if (!(ema_alpha > 0.0 && ema_alpha <= 1.0)) return set_error(SBVR_ERR_INVALID_ARG, "ema_alpha outside (0, 1]");
   return launch_encode_weights(cfg, W, dtype, M, N, out, group_mse, cache_size, ema_alpha, group_hit,
@@ -176,6 +213,17 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
   if (s != SBVR_OK) return s;
   if (!Y) return set_error(SBVR_ERR_INVALID_ARG, "Y is NULL");
   cudaStream_t st = (cudaStream_t)stream;
+  if (w->meta_kind == SBVR_META_INDEXED) {
+    // table + index weights: the mma.sync kernel (every SBVR-x form), K 2..4
+    if (X->kind != SBVR_ACT_SBVR) return set_error(SBVR_ERR_UNSUPPORTED, "indexed weights need an SBVR-x activation");
+    if (w->K < 2 || w->K > 4) return set_error(SBVR_ERR_UNSUPPORTED, "indexed weights: K=%d outside 2..4", w->K);
+    if (algo != SBVR_ALGO_AUTO && algo != SBVR_ALGO_MMA)
+      return set_error(SBVR_ERR_UNSUPPORTED, "indexed weights run on the MMA kernel, not algo %d", algo);
+    size_t need = mma_workspace_bytes(w, T);
+    if (need && (!workspace || ws_bytes < need))
+      return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    return launch_gemv_mma(w, X, T, Y, workspace, ws_bytes, nullptr, st);
+  }
   if (X->kind == SBVR_ACT_FP16) {
     // fp16-x: MMA (mma.m16n8k16 f16, tokens as MMA columns) by default; POPC selects the CUDA-core
     // reference kernel (one predicated add per set bit)
@@ -234,6 +282,8 @@ sbvr_status sbvr_gemv_to_peers(const sbvr_weights* w, const sbvr_act* X, int32_t
   s = check_act(w, X, T);
   if (s != SBVR_OK) return s;
   if (!peer_y) return set_error(SBVR_ERR_INVALID_ARG, "peer_y is NULL");
+  if (w->meta_kind == SBVR_META_INDEXED && (X->kind != SBVR_ACT_SBVR || w->K < 2 || w->K > 4))
+    return set_error(SBVR_ERR_UNSUPPORTED, "indexed weights need SBVR-x and K 2..4");
   if (n_peers < 1 || n_peers > 8) return set_error(SBVR_ERR_INVALID_ARG, "n_peers=%d outside 1..8", n_peers);
   if (y_row_offset < 0 || M_full < w->M || y_row_offset > M_full - w->M)
     return set_error(SBVR_ERR_SHAPE, "rows [%d, %d) do not fit M_full=%d", y_row_offset, y_row_offset + w->M, M_full);
@@ -274,6 +324,10 @@ sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_
   if (s != SBVR_OK) return s;
   if (!P) return set_error(SBVR_ERR_INVALID_ARG, "P is NULL");
   if (x->kind != SBVR_ACT_SBVR) return set_error(SBVR_ERR_INVALID_ARG, "partials need an SBVR activation");
+  if (w->meta_kind == SBVR_META_INDEXED && algo != SBVR_ALGO_MMA && algo != SBVR_ALGO_AUTO)
+    return set_error(SBVR_ERR_UNSUPPORTED, "indexed weights run on the MMA kernel");
+  if (w->meta_kind == SBVR_META_INDEXED && (w->K < 2 || w->K > 4))
+    return set_error(SBVR_ERR_UNSUPPORTED, "indexed weights: K=%d outside 2..4", w->K);
   if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, x, 1, nullptr, P, (cudaStream_t)stream);
   if (algo == SBVR_ALGO_TC) return launch_gemv_tc(w, x, 1, nullptr, nullptr, 0, P, (cudaStream_t)stream);
   if (algo == SBVR_ALGO_MMA || algo == SBVR_ALGO_AUTO)
@@ -288,6 +342,7 @@ sbvr_status sbvr_debug_zt_sums(const sbvr_weights* w, const sbvr_act* x, int32_t
   s = check_act(w, x, T);
   if (s != SBVR_OK) return s;
   if (!Tsum) return set_error(SBVR_ERR_INVALID_ARG, "Tsum is NULL");
+  if (w->meta_kind != SBVR_META_GROUP) return set_error(SBVR_ERR_UNSUPPORTED, "ZT reads SBVR_META_GROUP weights");
   if (T > 32) return set_error(SBVR_ERR_SHAPE, "T=%d: the debug export covers one pass (T <= 32)", T);
   if (!zt_supported(w, x)) return set_error(SBVR_ERR_UNSUPPORTED, "ZT needs SBVR-x and K <= 4");
   return launch_gemv_zt(w, x, T, nullptr, nullptr, 0, Tsum, (cudaStream_t)stream);
@@ -336,6 +391,38 @@ sbvr_status sbvr_unpack_canonical(int32_t M, int32_t N, int32_t K, int32_t group
       s16[q] = (uint16_t)(sb & 0xffffu);
       b16[q] = (uint16_t)(sb >> 16);
       r_idx[q] = data[Lo.ri_byte(r, g)];
+    }
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_pack_indexed(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint32_t* planes_canon,
+                              const uint8_t* idx, uint8_t* data) {
+  sbvr_status s = check_pack_args(M, N, K, group_size);
+  if (s != SBVR_OK) return s;
+  if (!planes_canon || !idx || !data) return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  IdxLayout Lo(M, N, K);
+  for (int r = 0; r < M; ++r)
+    for (int g = 0; g < Lo.NG; ++g) {
+      long q = (long)r * Lo.NG + g;
+      for (int t = 0; t < K; ++t)
+        for (int c = 0; c < kWPG; ++c) memcpy(data + Lo.plane_byte(r, g, t, c), planes_canon + (q * K + t) * kWPG + c, 4);
+      data[Lo.idx_byte(r, g)] = idx[q];
+    }
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_unpack_indexed(int32_t M, int32_t N, int32_t K, int32_t group_size, const uint8_t* data,
+                                uint32_t* planes_canon, uint8_t* idx) {
+  sbvr_status s = check_pack_args(M, N, K, group_size);
+  if (s != SBVR_OK) return s;
+  if (!planes_canon || !idx || !data) return set_error(SBVR_ERR_INVALID_ARG, "NULL pointer");
+  IdxLayout Lo(M, N, K);
+  for (int r = 0; r < M; ++r)
+    for (int g = 0; g < Lo.NG; ++g) {
+      long q = (long)r * Lo.NG + g;
+      for (int t = 0; t < K; ++t)
+        for (int c = 0; c < kWPG; ++c) memcpy(planes_canon + (q * K + t) * kWPG + c, data + Lo.plane_byte(r, g, t, c), 4);
+      idx[q] = data[Lo.idx_byte(r, g)];
     }
   return SBVR_OK;
 }

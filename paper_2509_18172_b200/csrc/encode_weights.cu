@@ -354,6 +354,150 @@ __global__ void __launch_bounds__(256) encode_weights_cached_kernel(EncParams p)
   }
 }
 
+// ---------------------------------------------------------------- f2: coefficient table + per-group index
+// (reading A23).  Step 1: Algorithm 1 on the evenly spaced sample groups; their winners are
+// written to cand[2i] = s16 | b16 << 16, cand[2i + 1] = r index.
+template <int K>
+__global__ void __launch_bounds__(256) encode_sample_kernel(EncParams p, int n_sample, uint32_t* cand) {
+  extern __shared__ double smem[];
+  GroupSmem sm;
+  sm.X = smem;
+  sm.Xs = sm.X + kG;
+  sm.R = sm.Xs + kG;
+  sm.S = sm.R + 64;
+  sm.B = sm.S + p.n_scale;
+  __shared__ double s_scal[4];
+  __shared__ double red_mse[8];
+  __shared__ int red_e[8];
+  __shared__ int win_e;
+  __shared__ double win_mse;
+  const int tid = threadIdx.x;
+  const int NG = p.N / kG;
+  const long n_groups = (long)p.M * NG;
+  const int SB = p.n_scale * p.n_bias;
+  for (int i = tid; i < p.n_ratio; i += blockDim.x) sm.R[i] = ratio_value(i, p.n_ratio);
+  for (int i = blockIdx.x; i < n_sample; i += gridDim.x) {
+    const long q = (long)i * n_groups / n_sample;
+    const int row = (int)(q / NG), g = (int)(q % NG);
+    grp_load(p, sm, row, g);
+    grp_candidates<K>(p, sm, s_scal);
+    grp_search<K>(p, sm, red_mse, red_e, &win_e, &win_mse);
+    if (tid == 0) {
+      const int we = win_e;
+      const int wi = we / SB, wrem = we - wi * SB, wj = wrem / p.n_bias, wk = wrem - wj * p.n_bias;
+      cand[2 * i] = (uint32_t)f64_to_f16_bits(sm.S[wj]) | ((uint32_t)f64_to_f16_bits(sm.B[wk]) << 16);
+      cand[2 * i + 1] = (uint32_t)wi;
+    }
+    __syncthreads();
+  }
+}
+
+// Step 2: the table = distinct sample winners in sample order (word 0 = entry count).
+__global__ void table_dedupe_kernel(const uint32_t* cand, int n_sample, uint32_t* table) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int n = 0;
+  for (int i = 0; i < n_sample; ++i) {
+    const uint32_t a = cand[2 * i], b = cand[2 * i + 1];
+    bool dup = false;
+    for (int j = 0; j < n && !dup; ++j) dup = table[1 + 2 * j] == a && table[2 + 2 * j] == b;
+    if (!dup) {
+      table[1 + 2 * n] = a;
+      table[2 + 2 * n] = b;
+      ++n;
+    }
+  }
+  table[0] = (uint32_t)n;
+}
+
+// Step 3: every group takes the table entry of least MSE (strict '<' in table order = a CTA arg-min on
+// (mse, entry)); its bits are assigned for that entry and stored in the indexed layout.
+template <int K>
+__global__ void __launch_bounds__(256) encode_indexed_kernel(EncParams p, const uint32_t* table) {
+  constexpr int NPTS = 1 << K;
+  __shared__ double X[kG];
+  __shared__ double R[64];
+  __shared__ double red_mse[8];
+  __shared__ int red_e[8];
+  __shared__ int win_e;
+  __shared__ double win_mse;
+  __shared__ uint32_t s_tab[2 * kMaxTable];
+  __shared__ int s_n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const IdxLayout Lo(p.M, p.N, K);
+  const long n_groups = (long)p.M * Lo.NG;
+  for (int i = tid; i < p.n_ratio; i += blockDim.x) R[i] = ratio_value(i, p.n_ratio);
+  if (tid == 0) s_n = (int)table[0];
+  __syncthreads();
+  for (int i = tid; i < 2 * s_n; i += blockDim.x) s_tab[i] = table[1 + i];
+  __syncthreads();
+  const int n = s_n;
+  for (long q = blockIdx.x; q < n_groups; q += gridDim.x) {
+    const int row = (int)(q / Lo.NG), g = (int)(q % Lo.NG);
+    if (tid < kG) X[tid] = load_w(p.W, p.dtype, (size_t)row * p.N + (size_t)g * kG + tid);
+    __syncthreads();
+    double best = DBL_MAX;
+    int best_e = 0x7fffffff;
+    for (int e = tid; e < n; e += blockDim.x) {
+      const uint32_t sb = s_tab[2 * e];
+      const double m = entry_mse<K>(X, R[s_tab[2 * e + 1]], f16_bits_to_f64((uint16_t)(sb & 0xffffu)),
+                                    f16_bits_to_f64((uint16_t)(sb >> 16)));
+      if (m < best || (m == best && e < best_e)) { best = m; best_e = e; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double om = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
+      if (om < best || (om == best && oe < best_e)) { best = om; best_e = oe; }
+    }
+    if (lane == 0) { red_mse[warp] = best; red_e[warp] = best_e; }
+    __syncthreads();
+    if (tid == 0) {
+      double bm = red_mse[0];
+      int be = red_e[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (red_mse[w] < bm || (red_mse[w] == bm && red_e[w] < be)) { bm = red_mse[w]; be = red_e[w]; }
+      win_e = be;
+      win_mse = bm;
+    }
+    __syncthreads();
+    const int we = win_e;
+    const uint32_t sb = s_tab[2 * we];
+    const double r = R[s_tab[2 * we + 1]], s = f16_bits_to_f64((uint16_t)(sb & 0xffffu)),
+                 b = f16_bits_to_f64((uint16_t)(sb >> 16));
+    if (tid < kG) {
+      double c[K];
+      double pw = 1.0;
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        c[t] = __dadd_rn(__dmul_rn(s, pw), b);
+        pw = __dmul_rn(pw, r);
+      }
+      const double x = X[tid];
+      int bm = 0;
+      double bd = 0.0, bv = 0.0;
+#pragma unroll
+      for (int m = 0; m < NPTS; ++m) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < K; ++t)
+          if ((m >> t) & 1) acc = __dadd_rn(acc, c[t]);
+        const double d = fabs(__dsub_rn(x, acc));
+        if (m == 0 || d < bd || (d == bd && acc < bv)) { bd = d; bv = acc; bm = m; }
+      }
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        const uint32_t word = __ballot_sync(0xffffffffu, (bm >> t) & 1);
+        if (lane == t) *reinterpret_cast<uint32_t*>(p.data + Lo.plane_byte(row, g, t, warp)) = word;
+      }
+    }
+    if (tid == 0) {
+      p.data[Lo.idx_byte(row, g)] = (uint8_t)we;
+      if (p.group_mse) p.group_mse[(long)row * Lo.NG + g] = win_mse;
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void ratio_table_kernel(float* out, int n_ratio, int K) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_ratio) return;
@@ -412,6 +556,50 @@ sbvr_status launch_encode_weights(const sbvr_encode_config* cfg, const void* W, 
     case 4: s = launch_k<4>(p, cached, st); break;
     case 5: s = launch_k<5>(p, cached, st); break;
     case 6: s = launch_k<6>(p, cached, st); break;
+    default: return set_error(SBVR_ERR_UNSUPPORTED, "encoder K=%d", cfg->K);
+  }
+  if (s != SBVR_OK) return s;
+  return launch_ratio_table(out->ratio_pow, cfg->n_ratio, cfg->K, st);
+}
+
+template <int K>
+static sbvr_status launch_indexed_k(const EncParams& p, int n_sample, uint32_t* cand, uint32_t* table, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (2 * kG + 64 + p.n_scale + p.n_bias);
+  if (smem > 48 * 1024 - 2048) {
+    cudaError_t e = cudaFuncSetAttribute(encode_sample_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(e));
+  }
+  encode_sample_kernel<K><<<n_sample, 256, smem, st>>>(p, n_sample, cand);
+  sbvr_status s = check_launch("encode_sample_kernel");
+  if (s != SBVR_OK) return s;
+  table_dedupe_kernel<<<1, 32, 0, st>>>(cand, n_sample, table);
+  s = check_launch("table_dedupe_kernel");
+  if (s != SBVR_OK) return s;
+  const long groups = (long)p.M * (p.N / kG);
+  const int grid = (int)(groups < (1L << 30) ? groups : (1L << 30));
+  encode_indexed_kernel<K><<<grid, 256, 0, st>>>(p, table);
+  return check_launch("encode_indexed_kernel");
+}
+
+sbvr_status launch_encode_indexed(const sbvr_encode_config* cfg, int n_table, const void* W, int dtype, int M, int N,
+                                  const sbvr_weights* out, double* group_mse, uint32_t* cand, cudaStream_t st) {
+  EncParams p = {};
+  p.W = W; p.dtype = dtype; p.M = M; p.N = N;
+  p.n_ratio = cfg->n_ratio; p.n_scale = cfg->n_scale; p.n_bias = cfg->n_bias;
+  p.s_min_factor = cfg->s_min_factor;
+  p.data = out->data;
+  p.group_mse = group_mse;
+  p.cache_size = -1;
+  const long groups = (long)M * (N / kG);
+  const int n_sample = (int)(n_table < groups ? n_table : groups);
+  sbvr_status s;
+  switch (cfg->K) {
+    case 1: s = launch_indexed_k<1>(p, n_sample, cand, out->coef_table, st); break;
+    case 2: s = launch_indexed_k<2>(p, n_sample, cand, out->coef_table, st); break;
+    case 3: s = launch_indexed_k<3>(p, n_sample, cand, out->coef_table, st); break;
+    case 4: s = launch_indexed_k<4>(p, n_sample, cand, out->coef_table, st); break;
+    case 5: s = launch_indexed_k<5>(p, n_sample, cand, out->coef_table, st); break;
+    case 6: s = launch_indexed_k<6>(p, n_sample, cand, out->coef_table, st); break;
     default: return set_error(SBVR_ERR_UNSUPPORTED, "encoder K=%d", cfg->K);
   }
   if (s != SBVR_OK) return s;

@@ -97,6 +97,7 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
   p.M_full = peers ? peers->M_full : w->M;
   for (int j = 0; j < 8; ++j) p.peer_y[j] = peers && j < peers->n ? peers->y[j] : nullptr;
   p.ratio_pow = w->ratio_pow;
+  p.coef_table = w->meta_kind == SBVR_META_INDEXED ? w->coef_table : nullptr;
   p.units = w->data;
   p.K = w->K;
   p.n_full = w->M / kRowBlock;

@@ -77,6 +77,7 @@ constexpr unsigned int kSentinel = 0xFFFFFFFFu;   // "not yet written" (a NaN ar
 struct ImmaParams {
   const uint8_t* units;     // the weights' unit records (sbvr.h)
   const float* ratio_pow;   // [n_ratio][K]
+  const uint32_t* coef_table;   // SBVR_META_INDEXED: [1 + 2 n] (n, then (s16 | b16 << 16, ratio index)); else NULL
   const uint32_t* xplanes;  // [T][NG][l][4] (SBVR-x)
   const uint16_t* xh;       // [T][N] fp16 x (fp16-x path)
   int ntok;                 // fp16-x: tokens in this pass (<= 8, one per MMA column)
@@ -194,11 +195,11 @@ __device__ __forceinline__ int imad(int a, int b, int c) {
   return d;
 }
 
-template <int K, int NB>
+template <int K, int NB, bool IDX = false>
 struct Geom {
   static constexpr int kTileBytes = 256 * K;
   static constexpr int kPlaneBytes = NB * kTileBytes;
-  static constexpr int kSbBytes = NB * 64;
+  static constexpr int kSbBytes = IDX ? 0 : NB * 64;   // IDX (SBVR_META_INDEXED): no per-group s/b, a table index
   static constexpr int kRiBytes = NB * 16;
   static constexpr int kUnitBytes = kPlaneBytes + kSbBytes + kRiBytes;
   static constexpr int kSlotBytes = (kUnitBytes + 127) / 128 * 128;
@@ -229,39 +230,41 @@ __device__ __forceinline__ int unit_owner(int v, int qq, int rr) {
 // a band is the half h of row block rb: its planes, scale/bias and ratio indices are three
 // contiguous pieces of the (rb, g) unit record.  Tiles [i0, i1) of the band -> three bulk copies
 // into the slot at their full-unit offsets [planes][sb][ri].
-template <int K, int NB>
+template <int K, int NB, bool IDX = false>
 __device__ __forceinline__ void issue_unit(uint8_t* slot, uint64_t* bar, const ImmaParams& p, int band, int g,
                                            int i0, int i1) {
-  using Gm = Geom<K, NB>;
+  using Gm = Geom<K, NB, IDX>;
+  constexpr int kMeta = IDX ? 1 : 5;           // meta bytes per row: table index, or fp16 s, b + ratio index
   const int NG = p.N / kG;
   const int rb = band >> 1, h = band & 1;
   const int R = rb < p.n_full ? 128 : p.tail_rows;
-  const size_t ub = (size_t)R * (16 * K + 5);
+  const size_t ub = (size_t)R * (16 * K + kMeta);
   const uint8_t* u = rb < p.n_full ? p.units + ((size_t)rb * NG + g) * ub
-                                    : p.units + (size_t)p.n_full * NG * (128 * (16 * K + 5)) + (size_t)g * ub;
+                                    : p.units + (size_t)p.n_full * NG * (128 * (16 * K + kMeta)) + (size_t)g * ub;
   const int r0 = 64 * h + 16 * i0, nt = i1 - i0;
-  mbar_expect_tx(bar, nt * (Gm::kTileBytes + 64 + 16));
+  mbar_expect_tx(bar, nt * (Gm::kTileBytes + (IDX ? 16 : 64 + 16)));
   bulk_g2s(slot + i0 * Gm::kTileBytes, u + (size_t)r0 * 16 * K, nt * Gm::kTileBytes, bar);
-  bulk_g2s(slot + Gm::kPlaneBytes + 64 * i0, u + (size_t)R * 16 * K + 4 * r0, nt * 64, bar);
-  bulk_g2s(slot + Gm::kPlaneBytes + Gm::kSbBytes + 16 * i0, u + (size_t)R * (16 * K + 4) + r0, nt * 16, bar);
+  if (!IDX) bulk_g2s(slot + Gm::kPlaneBytes + 64 * i0, u + (size_t)R * 16 * K + 4 * r0, nt * 64, bar);
+  bulk_g2s(slot + Gm::kPlaneBytes + Gm::kSbBytes + 16 * i0, u + (size_t)R * (16 * K + kMeta - 1) + r0, nt * 16, bar);
 }
 
 // F16X: the fp16-x path (north star): M_t = sum_e beta_t[e] x_e with x in fp16, on
 // mma.m16n8k16 f16 (A = plane bits as 0/1.0 pairs, B = the lane's own x values, columns = tokens);
 // TT is then the number of token columns kept (<= 8).
-template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB>
+template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB, bool IDX>
 #ifdef SBVR_MMA_MAXNREG
 __global__ void __maxnreg__(SBVR_MMA_MAXNREG) gemv_mma_kernel(ImmaParams p) {
 #else
 __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams p) {
 #endif
-  using Gm = Geom<K, NB>;
+  using Gm = Geom<K, NB, IDX>;
   constexpr int PTC = (NB % 2 == 0 && ((TT == 1 && !F16X) || ZB)) ? 2 : 1;   // tiles per compute step
   constexpr int NACC = (F16X || ZB) ? 2 : TT;          // accumulators per tile: tokens (SBVR) or columns (F16X, ZB)
   constexpr int NMMA = ZB ? 1 : TT;                    // MMAs per (tile, plane, slice pair)
   constexpr int kSumBatch = kSumBatchMax / (TT >= 4 ? 4 : TT);   // keep the pulled words <= 16 per lane
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ float s_rat[64];                 // r_i (fp32) for the Horner evaluation of sum_t r^t u_t
+  __shared__ __align__(8) uint32_t s_tab[IDX ? 2 * 256 : 2];   // IDX: coefficient table (fp16 s | b << 16, r fp32)
   __shared__ uint64_t s_bar[kImmaWarps][kSlots];
   __shared__ unsigned int s_cnt[2 * kImmaWarps];  // warps done with a band, by (first warp, its first/last band)
   __shared__ int s_fb[kImmaWarps];                 // first launch-local band of each warp
@@ -297,7 +300,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
   auto issue_next = [&](uint8_t* slot_ptr, uint64_t* bar, int kk) {
     int i0, i1;
     tiles_of(kk, i0, i1);
-    issue_unit<K, NB>(slot_ptr, bar, p, p.band0 + ib_band, ib_g, i0, i1);
+    issue_unit<K, NB, IDX>(slot_ptr, bar, p, p.band0 + ib_band, ib_g, i0, i1);
     if (++ib_g == NG) { ib_g = 0; ++ib_band; }
   };
   if (n_mine > 0 && lane == 0) {
@@ -310,6 +313,12 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
       if (s2 < n_mine && !EXPM(2)) issue_next(ring + s2 * Gm::kSlotBytes, bars + s2, s2);
   }
   for (int i = threadIdx.x; i < p.n_ratio; i += blockDim.x) s_rat[i] = K >= 2 ? p.ratio_pow[i * K + 1] : 0.f;
+  if constexpr (IDX)      // entry e -> (fp16 s | b << 16, r as fp32 bits): one 8-byte shared load per row and tile
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+      const bool live = i < (int)p.coef_table[0];
+      s_tab[2 * i] = live ? p.coef_table[1 + 2 * i] : 0u;
+      s_tab[2 * i + 1] = live ? __float_as_uint(K >= 2 ? p.ratio_pow[p.coef_table[2 + 2 * i] * K + 1] : 0.f) : 0u;
+    }
   for (int i = threadIdx.x; i < 2 * kImmaWarps; i += blockDim.x) s_cnt[i] = 0u;
   if (threadIdx.x < kImmaWarps) {
     const int w2 = threadIdx.x;
@@ -490,10 +499,18 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
           w[j][2 * t] = *reinterpret_cast<const uint32_t*>(ra + 16 * (t ^ swz_a));
           w[j][2 * t + 1] = *reinterpret_cast<const uint32_t*>(rb8 + 16 * (t ^ swz_b));
         }
-        sb0[j] = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq) * 4);
-        sb1[j] = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq + 8) * 4);
-        r2[j] = make_float2(s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq]],
-                            s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq + 8]]);
+        if constexpr (IDX) {
+          const int x0 = sl[Gm::kPlaneBytes + 16 * i + gq], x1 = sl[Gm::kPlaneBytes + 16 * i + gq + 8];
+          const uint2 e0 = reinterpret_cast<const uint2*>(s_tab)[x0], e1 = reinterpret_cast<const uint2*>(s_tab)[x1];
+          sb0[j] = e0.x;
+          sb1[j] = e1.x;
+          r2[j] = make_float2(__uint_as_float(e0.y), __uint_as_float(e1.y));
+        } else {
+          sb0[j] = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq) * 4);
+          sb1[j] = *reinterpret_cast<const uint32_t*>(sl + Gm::kPlaneBytes + (16 * i + gq + 8) * 4);
+          r2[j] = make_float2(s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq]],
+                              s_rat[sl[Gm::kPlaneBytes + Gm::kSbBytes + 16 * i + gq + 8]]);
+        }
       }
 
       if constexpr (F16X) {
@@ -899,13 +916,13 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
 #endif
 }
 
-template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB = false>
+template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB = false, bool IDX = false>
 inline cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
-  const int smem = kImmaWarps * Geom<K, NB>::kWarpBytes + kImmaWarps * 2 * TT * 64 * 4;
+  const int smem = kImmaWarps * Geom<K, NB, IDX>::kWarpBytes + kImmaWarps * 2 * TT * 64 * 4;
   static bool attr[64] = {false};     // the attribute is per device
   const int dev = cur_device();
   if (dev < 0 || dev >= 64 || !attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB>,
+    cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB, IDX>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr[dev] = true;
@@ -923,11 +940,21 @@ inline cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
   attr_pdl[1].val.cooperative = coop;
   cfg.attrs = attr_pdl;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB>, p);
+  return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB, IDX>, p);
 }
 
 template <int K, int NB>
 inline cudaError_t launch_nb(const ImmaParams& p, int TT, bool debug, bool f16x, bool zb, cudaStream_t st) {
+  if (p.coef_table) {                      // SBVR_META_INDEXED weights: SBVR-x forms, K 2..4 (checked by the ABI)
+    if constexpr (K >= 2 && K <= 4) {
+      if (zb) return launch_one<K, NB, 8, false, false, true, true>(p, st);
+      if (debug) return launch_one<K, NB, 1, true, false, false, true>(p, st);
+      if (TT == 1) return launch_one<K, NB, 1, false, false, false, true>(p, st);
+      if (TT == 2) return launch_one<K, NB, 2, false, false, false, true>(p, st);
+      return launch_one<K, NB, 4, false, false, false, true>(p, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (zb) return launch_one<K, NB, 8, false, false, true>(p, st);
   if (f16x) {
     switch (TT) {

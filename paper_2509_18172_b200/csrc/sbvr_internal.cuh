@@ -60,6 +60,35 @@ struct Layout {
   }
 };
 
+// SBVR_META_INDEXED records: [R x 16K planes][R x 1 B coefficient-table index]
+struct IdxLayout {
+  int M, N, K, NG, n_full, tail_rows;
+  __host__ __device__ IdxLayout(int M_, int N_, int K_) : M(M_), N(N_), K(K_) {
+    NG = N / kG;
+    n_full = M / kRowBlock;
+    tail_rows = M % kRowBlock;
+  }
+  __host__ __device__ int rows_in(int rb) const { return rb < n_full ? kRowBlock : tail_rows; }
+  __host__ __device__ long unit_bytes(int rows) const { return (long)rows * (16L * K + 1); }
+  __host__ __device__ long unit_off(int rb, int g) const {
+    if (rb < n_full) return ((long)rb * NG + g) * unit_bytes(kRowBlock);
+    return (long)n_full * NG * unit_bytes(kRowBlock) + (long)g * unit_bytes(tail_rows);
+  }
+  __host__ __device__ long total_bytes() const {
+    return (long)n_full * NG * unit_bytes(kRowBlock) + (tail_rows ? (long)NG * unit_bytes(tail_rows) : 0L);
+  }
+  __host__ __device__ long plane_byte(int row, int g, int t, int c) const {
+    const int rb = row / kRowBlock, r = row % kRowBlock;
+    return unit_off(rb, g) + (long)r * 16 * K + 16 * (t ^ chunk_swizzle(K, r)) + 4 * c;
+  }
+  __host__ __device__ long idx_byte(int row, int g) const {
+    const int rb = row / kRowBlock, r = row % kRowBlock;
+    return unit_off(rb, g) + (long)rows_in(rb) * 16 * K + r;
+  }
+};
+constexpr int kMaxTable = 256;
+constexpr size_t kTableBytes = (1 + 2 * kMaxTable) * 4;
+
 // ------------------------------------------------------------------ error plumbing
 sbvr_status set_error(sbvr_status s, const char* fmt, ...);
 sbvr_status check_launch(const char* what);
@@ -71,6 +100,8 @@ sbvr_status launch_encode_weights(const sbvr_encode_config* cfg, const void* W, 
                                   const sbvr_weights* out, double* group_mse, int cache_size, double cache_alpha,
                                   uint8_t* group_hit, cudaStream_t st);
 sbvr_status launch_ratio_table(float* ratio_pow, int n_ratio, int K, cudaStream_t st);
+sbvr_status launch_encode_indexed(const sbvr_encode_config* cfg, int n_table, const void* W, int dtype, int M, int N,
+                                  const sbvr_weights* out, double* group_mse, uint32_t* cand, cudaStream_t st);
 sbvr_status launch_gemv_popc(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, int32_t* P_debug,
                              cudaStream_t st);
 sbvr_status launch_gemv_fp16x(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, cudaStream_t st);

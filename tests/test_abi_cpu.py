@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 15
     for s in syms:
         assert hasattr(L, s), s
-    assert L.sbvr_abi_version() == 1
+    assert L.sbvr_abi_version() == 2
     assert L.sbvr_status_string(2) == b"SBVR_ERR_SHAPE"
 
 
@@ -117,3 +117,21 @@ def test_algorithmic_bytes_match_survey_table():
     # SURVEY §8d.3 table (fp16-x path): q/o 4096x4096 K=4 -> 9,068,544 B; down 4096x14336 -> 31,698,944 B
     assert sb.algorithmic_bytes(4096, 4096, 4, act="fp16") == 9068544
     assert sb.algorithmic_bytes(4096, 14336, 4, act="fp16") == 31698944
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 128, 4), (80, 384, 3), (208, 512, 2)])
+def test_indexed_pack_unpack_roundtrip_and_size(M, N, K):
+    """SBVR_META_INDEXED layout: 1 byte of meta per group (P:246 coefficient index) instead of 5."""
+    pc, _, _, _ = synthetic.random_encoded(M, N, K, 16, seed=M + K)
+    idx = np.random.default_rng(M).integers(0, 256, size=(M, N // 128)).astype(np.uint8)
+    db, rpb, tb = sb.weights_bytes_ex(M, N, K, 16, sb.META_INDEXED)
+    assert db == M * N * K // 8 + M * (N // 128) and tb == (1 + 2 * 256) * 4
+    data = np.zeros(db, np.uint8)
+    L = sb.lib()
+    assert L.sbvr_pack_indexed(M, N, K, 128, sb._np_ptr(np.ascontiguousarray(pc)), sb._np_ptr(idx), sb._np_ptr(data)) == 0
+    pc2 = np.zeros_like(pc)
+    idx2 = np.zeros_like(idx)
+    assert L.sbvr_unpack_indexed(M, N, K, 128, sb._np_ptr(data), sb._np_ptr(pc2), sb._np_ptr(idx2)) == 0
+    assert np.array_equal(pc, pc2) and np.array_equal(idx, idx2)
+    src = np.concatenate([pc.reshape(-1).view(np.uint8), idx.reshape(-1)])
+    assert np.array_equal(np.sort(data), np.sort(src))
