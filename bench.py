@@ -273,6 +273,9 @@ def run_sbvr(args, world, rank, local_rank, pg):
                 cr.record_external(events[j][0], stream)
             if symm is not None:                        # all-gather fused into the GEMV epilogue (dist.py)
                 symm[r][j](acts[xin])
+            elif args.chain:                         # + L2 prefetch of the next GEMV's first units (next layer's qkv last)
+                nxt = layers[r][j + 1][5] if j + 1 < len(layers[r]) else layers[(r + 1) % ring][0][5]
+                sb.gemv_chain(w, acts[xin], nxt, y=ys[r][j], ws=ws)
             else:
                 sb.gemv(w, acts[xin], y=ys[r][j], ws=ws)
             if events is not None:
@@ -740,6 +743,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="sbvr", choices=["sbvr", "reference"])
     ap.add_argument("--ring", type=int, default=4)
+    ap.add_argument("--chain", action="store_true",
+                    help="launch the step's GEMVs with sbvr_gemv_chain (L2 prefetch of the next GEMV's first units; "
+                         "measured no gain: profiles/r02_chain_ab.txt)")
     ap.add_argument("--allgather", default="nccl", choices=["nccl", "symm"],
                     help="N > 1: join y with an NCCL all-gather, or store it to every rank from the GEMV epilogue "
                          "(symmetric memory, dist.SymmRowShardedGemv)")

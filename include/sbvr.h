@@ -213,6 +213,15 @@ sbvr_status sbvr_gemv(const sbvr_weights* w, const sbvr_act* x, float* y, void* 
 sbvr_status sbvr_gemv_batched(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
                               size_t ws_bytes, void* stream);
 
+/* sbvr_gemv_chain -- sbvr_gemv_batched plus a hint naming the weights of the GEMV that the caller launches next on
+ * the same stream (e.g. the next projection of a decoder layer, or the next layer's first).  Results are identical
+ * to sbvr_gemv_batched; the hint only moves data: once a CTA has issued its last weight copy, it prefetches into
+ * L2 the first unit records that CTA index will copy first in a GEMV over next_w, so the next launch's pipeline
+ * fill hits L2 instead of waiting on HBM (B200 126 MB L2).  next_w may be NULL (= sbvr_gemv_batched); it is only
+ * read as addresses and shape (SBVR_META_GROUP weights; ignored for other kinds). */
+sbvr_status sbvr_gemv_chain(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
+                            size_t ws_bytes, const sbvr_weights* next_w, void* stream);
+
 /* sbvr_gemv_to_peers -- the row-sharded multi-GPU GEMV with the all-gather fused into its epilogue (north star
  * "row-sharded multi-GPU path ... joins y").  W is this rank's row shard (rows
  * [y_row_offset, y_row_offset + W.M) of an M_full-row matrix); every y value the kernel produces is stored, over

@@ -92,6 +92,8 @@ def lib():
                          ("sbvr_unpack_indexed", [i32, i32, i32, i32, P, P, P])):
             if hasattr(L, name):
                 getattr(L, name).argtypes = at
+        if hasattr(L, "sbvr_gemv_chain"):
+            L.sbvr_gemv_chain.argtypes = [P, P, i32, P, P, sz, P, P]
         if hasattr(L, "sbvr_gemv_to_peers"):
             L.sbvr_gemv_to_peers.argtypes = [P, P, i32, P, i32, i32, i32, P, sz, P]
         # (A/B timing loads older builds through SBVR_LIB_AB: symbols they lack are simply not declared)
@@ -99,7 +101,7 @@ def lib():
                      "sbvr_workspace_init", "sbvr_gemv", "sbvr_gemv_batched", "sbvr_gemv_ex", "sbvr_debug_partials",
                      "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows", "sbvr_encode_weights_cached",
                      "sbvr_debug_zt_sums", "sbvr_gemv_to_peers", "sbvr_weights_bytes_ex",
-                     "sbvr_encode_weights_indexed", "sbvr_pack_indexed", "sbvr_unpack_indexed"):
+                     "sbvr_encode_weights_indexed", "sbvr_pack_indexed", "sbvr_unpack_indexed", "sbvr_gemv_chain"):
             if hasattr(L, name):
                 getattr(L, name).restype = i32
         _lib = L
@@ -343,6 +345,21 @@ def gemv(w: SbvrWeights, x: SbvrActivation, y: Optional[torch.Tensor] = None,
     wd, xd = w.desc(), x.desc()
     _check(lib().sbvr_gemv(ctypes.byref(wd), ctypes.byref(xd), _ptr(y), _ptr(ws.buf), ws.nbytes, _stream()),
            "sbvr_gemv")
+    return y
+
+
+def gemv_chain(w: SbvrWeights, x: SbvrActivation, next_w: Optional[SbvrWeights], y: Optional[torch.Tensor] = None,
+               ws: Optional[Workspace] = None) -> torch.Tensor:
+    """sbvr_gemv_chain: as gemv/gemv_batched, plus the L2-prefetch hint for the GEMV over next_w launched next."""
+    T = x.T
+    if y is None:
+        y = torch.empty((T, w.M) if T > 1 else (w.M,), dtype=torch.float32, device=w.data.device)
+    if ws is None:
+        ws = Workspace.for_weights(w, T)
+    wd, xd = w.desc(), x.desc()
+    nd = next_w.desc() if next_w is not None else None
+    _check(lib().sbvr_gemv_chain(ctypes.byref(wd), ctypes.byref(xd), T, _ptr(y), _ptr(ws.buf), ws.nbytes,
+                                 ctypes.byref(nd) if nd is not None else None, _stream()), "sbvr_gemv_chain")
     return y
 
 

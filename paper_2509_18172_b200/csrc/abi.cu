@@ -274,6 +274,27 @@ sbvr_status sbvr_gemv(const sbvr_weights* w, const sbvr_act* x, float* y, void* 
   return sbvr_gemv_ex(w, x, 1, y, workspace, ws_bytes, SBVR_ALGO_AUTO, stream);
 }
 
+sbvr_status sbvr_gemv_chain(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
+                            size_t ws_bytes, const sbvr_weights* next_w, void* stream) {
+  if (!next_w) return sbvr_gemv_batched(w, X, T, Y, workspace, ws_bytes, stream);
+  sbvr_status s = check_weights(next_w);
+  if (s != SBVR_OK) return s;
+  s = check_weights(w);
+  if (s != SBVR_OK) return s;
+  s = check_act(w, X, T);
+  if (s != SBVR_OK) return s;
+  if (!Y) return set_error(SBVR_ERR_INVALID_ARG, "Y is NULL");
+  // the hint is honoured by the mma.sync kernel (batch 1-2 and its batched forms); elsewhere it is ignored
+  const bool mma = X->kind == SBVR_ACT_SBVR && (w->meta_kind == SBVR_META_INDEXED ? (w->K >= 2 && w->K <= 4) : true);
+  static const int zt_min = getenv("SBVR_ZT_MIN_T") ? atoi(getenv("SBVR_ZT_MIN_T")) : 12;
+  if (!mma || (w->meta_kind == SBVR_META_GROUP && T >= zt_min && zt_supported(w, X)))
+    return sbvr_gemv_batched(w, X, T, Y, workspace, ws_bytes, stream);
+  size_t need = mma_workspace_bytes(w, T);
+  if (need && (!workspace || ws_bytes < need))
+    return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+  return launch_gemv_mma(w, X, T, Y, workspace, ws_bytes, nullptr, (cudaStream_t)stream, nullptr, next_w);
+}
+
 sbvr_status sbvr_gemv_to_peers(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* const* peer_y,
                                int32_t n_peers, int32_t y_row_offset, int32_t M_full, void* workspace, size_t ws_bytes,
                                void* stream) {

@@ -89,9 +89,22 @@ static cudaError_t launch_any(int K, const ImmaParams& p, int NB, int TT, bool d
 size_t mma_workspace_bytes(const sbvr_weights* w, int T) { return mma_workspace_bytes_(w, T); }
 
 sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
-                            int32_t* P_debug, cudaStream_t st, const PeerOut* peers) {
+                            int32_t* P_debug, cudaStream_t st, const PeerOut* peers, const sbvr_weights* next_w) {
   const Plan pl = make_plan(w);
   ImmaParams p;
+  p.nx_units = nullptr;
+  if (next_w && next_w->meta_kind == SBVR_META_GROUP) {
+    const Plan nx = make_plan(next_w);
+    if (nx.Us_main > 0) {
+      p.nx_units = next_w->data;
+      p.nx_NG = nx.NG;
+      p.nx_K = next_w->K;
+      p.nx_Us = nx.Us_main;
+      p.nx_C = nx.C_main;
+      p.nx_qq = nx.Us_main / nx.C_main;
+      p.nx_rr = nx.Us_main % nx.C_main;
+    }
+  }
   p.n_peers = peers ? peers->n : 0;
   p.y_off = peers ? peers->row_offset : 0;
   p.M_full = peers ? peers->M_full : w->M;
@@ -150,7 +163,10 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
       // step at the end of a launch, a lone tile half of it (measured on the bench step: +0.7 %, the
       // big GEMVs 1.5 % faster; a pair-granular split for small problems measured no better)
       p.fine = 1;
+      const uint8_t* nx_keep = p.nx_units;
+      if (part != 0 || done + ntok < T) p.nx_units = nullptr;     // the hint belongs to the last pass, main launch
       cudaError_t e = launch_any(w->K, p, NB, TT, debug, f16x, zb, st);
+      p.nx_units = nx_keep;
       if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "gemv_mma setup: %s", cudaGetErrorString(e));
       sbvr_status s = check_launch("gemv_mma_kernel");
       if (s != SBVR_OK) return s;

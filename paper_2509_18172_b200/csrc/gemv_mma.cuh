@@ -95,6 +95,9 @@ struct ImmaParams {
   int Us;                   // units in this launch
   int Pw, qq, rr;           // CTAs and the unit partition over CTAs
   int one;                  // = 1 (runtime value, see i2f_fma)
+  // chain hint (sbvr_gemv_chain): the next GEMV's weights and its work partition (main launch), or NULL
+  const uint8_t* nx_units;
+  int nx_NG, nx_K, nx_Us, nx_C, nx_qq, nx_rr;
   int fine;                 // 1: warp ranges at single-tile granularity (large problems: the last step of a
                             // warp may be a lone tile); 0: whole tile pairs (small problems keep the ILP)
   int exp;                  // ablation bits (env SBVR_EXP_MODE, 0 in production): 1 skip the tile
@@ -246,6 +249,32 @@ __device__ __forceinline__ void issue_unit(uint8_t* slot, uint64_t* bar, const I
   bulk_g2s(slot + i0 * Gm::kTileBytes, u + (size_t)r0 * 16 * K, nt * Gm::kTileBytes, bar);
   if (!IDX) bulk_g2s(slot + Gm::kPlaneBytes + 64 * i0, u + (size_t)R * 16 * K + 4 * r0, nt * 64, bar);
   bulk_g2s(slot + Gm::kPlaneBytes + Gm::kSbBytes + 16 * i0, u + (size_t)R * (16 * K + kMeta - 1) + r0, nt * 16, bar);
+}
+
+// L2 prefetch of the first two units warp wib of CTA c will copy in the next GEMV of a chain (same unit-record
+// layout and work split as this kernel's main launch, SBVR_META_GROUP): cp.async.bulk.prefetch.L2, no smem.
+// (scalar arguments only: taking the address of the kernel's parameter struct would move it to local memory)
+static __device__ __noinline__ void prefetch_next(const uint8_t* nx_units, int nx_NG, int K, int nx_C, int nx_qq,
+                                                  int nx_rr, int c, int wib) {
+  if (c >= nx_C) return;
+  const int V0 = c * nx_qq + min(c, nx_rr);
+  const int V1 = V0 + nx_qq + (c < nx_rr ? 1 : 0);
+  const int nTc = (V1 - V0) * 4;
+  const int tq = nTc / kImmaWarps, tr = nTc % kImmaWarps;
+  const int T0 = wib * tq + min(wib, tr), T1 = T0 + tq + (wib < tr ? 1 : 0);
+  if (T1 <= T0) return;
+  const size_t ub = (size_t)128 * (16 * K + 5);
+  for (int uu = V0 + T0 / 4; uu <= V0 + (T1 - 1) / 4 && uu < V0 + T0 / 4 + 2; ++uu) {
+    const int band = uu / nx_NG, g = uu - band * nx_NG;
+    const int rb = band >> 1, h = band & 1;
+    const uint8_t* u = nx_units + ((size_t)rb * nx_NG + g) * ub;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(u + (size_t)h * 64 * 16 * K), "r"(64 * 16 * K)
+                 : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(u + (size_t)128 * 16 * K + h * 256), "r"(256)
+                 : "memory");
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(u + (size_t)128 * (16 * K + 4) + h * 64), "r"(64)
+                 : "memory");
+  }
 }
 
 // F16X: the fp16-x path (north star): M_t = sum_e beta_t[e] x_e with x in fp16, on
@@ -683,6 +712,10 @@ __global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue_next(sl, bars + slot, k + kSlots);
     }
+    // this warp has issued its last weight copy: while HBM would drain, pull into L2 the first units that the
+    // same warp of the same CTA index fetches first in the next GEMV of the chain (sbvr_gemv_chain)
+    if (lane == 0 && p.nx_units && k + kSlots == (n_mine > kSlots ? n_mine : kSlots))
+      prefetch_next(p.nx_units, p.nx_NG, p.nx_K, p.nx_C, p.nx_qq, p.nx_rr, cta, wib);
     if (++slot == kSlots) { slot = 0; phase ^= 1u; }
 
     // ---- leaving band b.  Only a warp's first and last band can be shared with other warps of

@@ -114,7 +114,8 @@ struct PeerOut {
   int n, row_offset, M_full;
 };
 sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, float* Y, void* ws, size_t ws_bytes,
-                            int32_t* P_debug, cudaStream_t st, const PeerOut* peers = nullptr);
+                            int32_t* P_debug, cudaStream_t st, const PeerOut* peers = nullptr,
+                            const sbvr_weights* next_w = nullptr);
 size_t mma_workspace_bytes(const sbvr_weights* w, int T);
 sbvr_status launch_gemv_pipe(const sbvr_weights* w, const sbvr_act* x, float* y, void* ws, int32_t* P_debug,
                              cudaStream_t st);
