@@ -34,7 +34,7 @@ from paper_2509_18172_b200 import dist as sdist  # noqa: E402
 
 METRIC = "SBVR GEMV HBM GB/s (% of 8 TB/s) and µs/GEMV at 1/2/4/8 B200 vs fp16 cuBLAS"
 K_BITS, L_BITS, G, N_RATIO = 4, 8, 128, 16
-EV_EVERY = 8          # one timed step in EV_EVERY carries per-GEMV CUDA events (roofline durations)
+EV_EVERY = 32         # one timed step in EV_EVERY carries the CUDA-event span around its GEMV launches (roofline)
 # which activation feeds which projection: q,k,v <- x_attn; o <- x_o; gate,up <- x_mlp; down <- x_down
 INPUT_OF = {"q_proj": 0, "k_proj": 0, "v_proj": 0, "o_proj": 1, "gate_proj": 2, "up_proj": 2, "down_proj": 3}
 INPUT_N = [4096, 4096, 4096, 14336]

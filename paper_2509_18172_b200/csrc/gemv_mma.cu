@@ -40,7 +40,7 @@ struct Plan {
 // per kMinUnitsPerCta units.
 static int ctas_for(int Us, int NG) {
   if (Us <= 0) return 0;
-  int C = num_sms();
+  int C = num_sms() * SBVR_MMA_CTAS_PER_SM;
   const int cap = (Us + kMinUnitsPerCta - 1) / kMinUnitsPerCta;
   if (C > cap) C = cap;
   return C < 1 ? 1 : C;

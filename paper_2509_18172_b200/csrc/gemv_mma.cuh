@@ -32,7 +32,8 @@
 // number, y += s_x * (s * sum_t r^t u_t + b * sum_t u_t) (c_t = s r^t + b, Eq. 4);
 // alpha_{2c}/128 is applied when the quad is reduced (2 shuffles per row per band).
 //
-// Work split: units are split into contiguous, balanced ranges over CTAs (one 16-warp CTA per SM),
+// Work split: units are split into contiguous, balanced ranges over CTAs (two 8-warp CTAs per SM: when
+// one finishes, a CTA of the next launch starts its weight copies on that half SM while the other still runs),
 // and each CTA's tiles into contiguous warp ranges.  A band shared by several warps is summed in
 // warp order by the last warp to finish it (smem counter); a band shared by several CTAs by the
 // last CTA to finish it (global arrival counter; every contributor publishes its partial first):
@@ -58,10 +59,13 @@ inline int cur_device() {
 
 
 #ifndef SBVR_MMA_WARPS
-#define SBVR_MMA_WARPS 16
+#define SBVR_MMA_WARPS 8
 #endif
-constexpr int kImmaWarps = SBVR_MMA_WARPS;   // warps per CTA (one CTA per SM: the register file is full)
+constexpr int kImmaWarps = SBVR_MMA_WARPS;   // warps per CTA (two CTAs per SM fill the register file)
 constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at least this many units per CTA
+#ifndef SBVR_MMA_CTAS_PER_SM
+#define SBVR_MMA_CTAS_PER_SM 2     // resident CTAs per SM: two 8-warp CTAs (profiles/r02_cta_shape_ab.txt)
+#endif
 #ifndef SBVR_MMA_OWNER_PULL
 #define SBVR_MMA_OWNER_PULL 0
 #endif
@@ -284,7 +288,7 @@ template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB, bool IDX>
 #ifdef SBVR_MMA_MAXNREG
 __global__ void __maxnreg__(SBVR_MMA_MAXNREG) gemv_mma_kernel(ImmaParams p) {
 #else
-__global__ void __launch_bounds__(kImmaWarps * 32, 1) gemv_mma_kernel(ImmaParams p) {
+__global__ void __launch_bounds__(kImmaWarps * 32, SBVR_MMA_CTAS_PER_SM) gemv_mma_kernel(ImmaParams p) {
 #endif
   using Gm = Geom<K, NB, IDX>;
   constexpr int PTC = (NB % 2 == 0 && ((TT == 1 && !F16X) || ZB)) ? 2 : 1;   // tiles per compute step
