@@ -63,6 +63,14 @@ struct ZtParams {
   int Us, qq, rr;            // units, and their partition over CTAs
   unsigned long long* ts;    // diagnostics (-DSBVR_DIAG, env SBVR_TS_PTR): [CTA][32] per-phase SM-cycle totals
 };
+#ifndef ZT_CRIT_SPIN
+#define ZT_CRIT_SPIN 1    // 1: critical-path waits (issuer on A/B ready, expansion on A/B free) spin instead of backing off
+#endif
+#if ZT_CRIT_SPIN
+#define ZT_WAIT_CRIT(bar, ph) mbar_wait(bar, ph)
+#else
+#define ZT_WAIT_CRIT(bar, ph) mbar_wait_backoff(bar, ph)
+#endif
 #ifndef ZT_ABL
 #define ZT_ABL 0   // ablation bits (diagnostic builds only): 1 no B build, 2 no A expansion, 4 no MMAs, 8 no x loads
 #endif
@@ -173,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
       PH_DECL
       const uint32_t bbase = smem_u32(sB);
       for (int k = 0; k < n; ++k) {
-        mbar_wait_backoff(&bar_a[k & 1], (k >> 1) & 1);         // A_t / B of unit k are in place
+        ZT_WAIT_CRIT(&bar_a[k & 1], (k >> 1) & 1);              // A_t / B of unit k are in place
         PH(0);
         const int db = k % kDBuf;
         if (k >= kDBuf)                                          // the epilogue has read D_t[db] of unit k - kDBuf
@@ -218,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
     int rb = V0 / NG, g = V0 - (V0 / NG) * NG;
     for (int k = 0; k < n; ++k) {
       const int rows = rows_of(rb);
-      if (k >= 2) mbar_wait_backoff(&bar_abfree[k & 1], ((k - 2) >> 1) & 1);   // A_t[k&1], B[k&1] read by MMA(k-2)
+      if (k >= 2) ZT_WAIT_CRIT(&bar_abfree[k & 1], ((k - 2) >> 1) & 1);   // A_t[k&1], B[k&1] read by MMA(k-2)
       PH(0);
       if (bwarp && !(ZT_ABL & 1)) {
         uint32_t Z[8];
