@@ -866,7 +866,7 @@ def main():
                      "how": "algorithmic bytes per launch / average launch duration over the 4 back-to-back GEMV "
                             "launches of a step (= their summed bytes / the CUDA-event span around them; external "
                             f"event nodes in {res['span_n']} of the {K} timed steps, every {EV_EVERY}th); traffic "
-                            "= ncu dram read+write bytes per launch, same 4 launches (profiles/r01_ncu_traffic.json)",
+                            "= ncu dram read+write bytes per launch, same 4 launches (profiles/r02_ncu_traffic.json)",
                      "gemv_span_us": round(res["span_ms_avg"] * 1e3, 3),
                      "algorithmic_bytes_per_launch": round(tot_b / len(FUSED))},
         "per_gemv": per,

@@ -1,4 +1,4 @@
-"""Turn the ncu metrics CSV of one bench step's GEMV launches into profiles/r01_ncu_traffic.json.
+"""Turn the ncu metrics CSV of one bench step's GEMV launches into profiles/r02_ncu_traffic.json.
 usage: python tools/traffic_from_ncu.py gpurun_out/traffic.csv"""
 import csv
 import json
@@ -48,5 +48,5 @@ out["traffic_over_algorithmic"] = round(tot_t / tot_a, 4)
 out["source"] = ("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control "
                  "none -k regex:gemv_mma on bench.py (first 4 GEMV launches = one step: qkv, o, gate_up, down)")
 json.dump(out, open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
-                                  "r01_ncu_traffic.json"), "w"), indent=1)
+                                  "r02_ncu_traffic.json"), "w"), indent=1)
 print(json.dumps(out, indent=1))
