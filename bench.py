@@ -251,6 +251,12 @@ def run_sbvr(args, world, rank, local_rank, pg):
             acts.append(sb.SbvrActivation(sb.ACT_SBVR, n, 1, L_BITS, act_all.data[g0 * L_BITS * 4:(g0 + ng) * L_BITS * 4],
                                           act_all.scales[g0:g0 + ng]))
             g0 += ng
+        if args.fused_conversion:                       # each GEMV converts its own input (Eq. 12 in its prologue)
+            e0 = 0
+            acts = []
+            for n in INPUT_N:
+                acts.append(sb.fp16q_activation(xs[0][e0:e0 + n], l=L_BITS))
+                e0 += n
         ys = [[torch.zeros(r1 - r0, dtype=torch.float32, device=device) for (_, M, N, r0, r1, w, ws, xin) in mats]
               for mats in layers]
         yfull = [torch.zeros(M, dtype=torch.float32, device=device) for (_, M, N, _, _) in FUSED]
@@ -265,7 +271,8 @@ def run_sbvr(args, world, rank, local_rank, pg):
         if e2e:
             for x, xh in zip(xs, xs_host):
                 x.copy_(xh, non_blocking=True)
-        sb.encode_vector(xs[0], out=act_all)
+        if not args.fused_conversion:
+            sb.encode_vector(xs[0], out=act_all)
         if span is not None:
             cr.record_external(span[0], stream)
         for j, (name, M, N, r0, r1, w, ws, xin) in enumerate(layers[r]):
@@ -743,6 +750,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="sbvr", choices=["sbvr", "reference"])
     ap.add_argument("--ring", type=int, default=4)
+    ap.add_argument("--fused-conversion", action="store_true",
+                    help="no sbvr_encode_vector launch: every GEMV converts its fp16 input in its prologue "
+                         "(SBVR_ACT_FP16_Q, bit-identical)")
     ap.add_argument("--chain", action="store_true",
                     help="launch the step's GEMVs with sbvr_gemv_chain (L2 prefetch of the next GEMV's first units; "
                          "measured no gain: profiles/r02_chain_ab.txt)")
@@ -819,7 +829,7 @@ def main():
         except Exception:
             traffic = None
     e2e_val = res["step_bytes"] / (res["e2e_ms"] / K * 1e-3) / 1e9
-    launches = K * (1 + len(FUSED))
+    launches = K * ((0 if args.fused_conversion else 1) + len(FUSED))
     sm = np.asarray(res["step_ms"]) * 1e3
     step_stats = {"us_median": round(float(np.median(sm)), 3), "us_p10": round(float(np.percentile(sm, 10)), 3),
                   "us_p90": round(float(np.percentile(sm, 90)), 3), "us_mean": round(float(sm.mean()), 3)}

@@ -76,7 +76,10 @@ typedef enum {
 } sbvr_status;
 
 typedef enum { SBVR_F32 = 0, SBVR_F16 = 1, SBVR_BF16 = 2 } sbvr_dtype;
-typedef enum { SBVR_ACT_FP16 = 0, SBVR_ACT_SBVR = 1 } sbvr_act_kind;
+/* Activation kinds.  SBVR_ACT_FP16_Q: fp16 x (data = uint16_t[N]) that the GEMV converts to SBVR-x itself, in its
+ * prologue, with exactly the arithmetic of sbvr_encode_vector (Eq. 12, l bits) -- the result is bit-identical to
+ * sbvr_encode_vector + sbvr_gemv on SBVR-x, without the separate conversion launch.  T = 1, MMA kernel, K 2..4. */
+typedef enum { SBVR_ACT_FP16 = 0, SBVR_ACT_SBVR = 1, SBVR_ACT_FP16_Q = 2 } sbvr_act_kind;
 
 /* GEMV algorithm selector for sbvr_gemv_ex / sbvr_debug_partials.
  *  AUTO  : the fastest implemented kernel for the activation kind and batch (measured; SBVR-x: MMA,

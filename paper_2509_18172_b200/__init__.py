@@ -24,7 +24,7 @@ _lib = None
 
 OK, ERR_INVALID_ARG, ERR_SHAPE, ERR_UNSUPPORTED, ERR_ALIGNMENT, ERR_CUDA, ERR_WORKSPACE = range(7)
 F32, F16, BF16 = 0, 1, 2
-ACT_FP16, ACT_SBVR = 0, 1
+ACT_FP16, ACT_SBVR, ACT_FP16_Q = 0, 1, 2
 ALGO_AUTO, ALGO_POPC, ALGO_TC, ALGO_MMA, ALGO_PIPE, ALGO_ZT = 0, 1, 2, 3, 4, 5
 META_GROUP, META_INDEXED = 0, 1
 G = 128
@@ -295,6 +295,15 @@ def encode_vector(x: torch.Tensor, l: int = 8, out: Optional[SbvrActivation] = N
     _check(lib().sbvr_encode_vector(_ptr(x2), T, N, G, l, _ptr(out.data), _ptr(out.scales), _stream()),
            "sbvr_encode_vector")
     return out
+
+
+def fp16q_activation(x: torch.Tensor, l: int = 8) -> SbvrActivation:
+    """An fp16 activation the GEMV converts to SBVR-x itself (Eq. 12 in the kernel prologue, bit-identical to
+    encode_vector; batch 1)."""
+    assert x.is_cuda and x.dtype == torch.float16 and x.is_contiguous()
+    x2 = x.view(1, -1) if x.dim() == 1 else x
+    assert x2.shape[0] == 1
+    return SbvrActivation(ACT_FP16_Q, x2.shape[1], 1, l, x2)
 
 
 def fp16_activation(x: torch.Tensor) -> SbvrActivation:

@@ -63,6 +63,11 @@ static sbvr_status check_act(const sbvr_weights* w, const sbvr_act* x, int T) {
     if (!aligned16(x->data)) return set_error(SBVR_ERR_ALIGNMENT, "activation planes must be 16-byte aligned");
   } else if (x->kind == SBVR_ACT_FP16) {
     if (!aligned16(x->data)) return set_error(SBVR_ERR_ALIGNMENT, "fp16 activation must be 16-byte aligned");
+  } else if (x->kind == SBVR_ACT_FP16_Q) {
+    if (x->l < 2 || x->l > 8) return set_error(SBVR_ERR_UNSUPPORTED, "l=%d outside 2..8", x->l);
+    if (T != 1) return set_error(SBVR_ERR_UNSUPPORTED, "in-kernel conversion (SBVR_ACT_FP16_Q) runs T = 1 (T=%d)", T);
+    if (w->K < 2 || w->K > 4) return set_error(SBVR_ERR_UNSUPPORTED, "SBVR_ACT_FP16_Q: K=%d outside 2..4", w->K);
+    if (!aligned16(x->data)) return set_error(SBVR_ERR_ALIGNMENT, "fp16 activation must be 16-byte aligned");
   } else {
     return set_error(SBVR_ERR_INVALID_ARG, "unknown activation kind %d", x->kind);
   }
@@ -213,6 +218,14 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
   if (s != SBVR_OK) return s;
   if (!Y) return set_error(SBVR_ERR_INVALID_ARG, "Y is NULL");
   cudaStream_t st = (cudaStream_t)stream;
+  if (X->kind == SBVR_ACT_FP16_Q) {
+    if (algo != SBVR_ALGO_AUTO && algo != SBVR_ALGO_MMA)
+      return set_error(SBVR_ERR_UNSUPPORTED, "in-kernel conversion runs on the MMA kernel, not algo %d", algo);
+    size_t need = mma_workspace_bytes(w, T);
+    if (need && (!workspace || ws_bytes < need))
+      return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
+    return launch_gemv_mma(w, X, T, Y, workspace, ws_bytes, nullptr, st);
+  }
   if (w->meta_kind == SBVR_META_INDEXED) {
     // table + index weights: the mma.sync kernel (every SBVR-x form), K 2..4
     if (X->kind != SBVR_ACT_SBVR) return set_error(SBVR_ERR_UNSUPPORTED, "indexed weights need an SBVR-x activation");
@@ -285,7 +298,8 @@ sbvr_status sbvr_gemv_chain(const sbvr_weights* w, const sbvr_act* X, int32_t T,
   if (s != SBVR_OK) return s;
   if (!Y) return set_error(SBVR_ERR_INVALID_ARG, "Y is NULL");
   // the hint is honoured by the mma.sync kernel (batch 1-2 and its batched forms); elsewhere it is ignored
-  const bool mma = X->kind == SBVR_ACT_SBVR && (w->meta_kind == SBVR_META_INDEXED ? (w->K >= 2 && w->K <= 4) : true);
+  const bool mma = (X->kind == SBVR_ACT_SBVR || X->kind == SBVR_ACT_FP16_Q) &&
+                   (w->meta_kind == SBVR_META_INDEXED ? (w->K >= 2 && w->K <= 4) : true);
   static const int zt_min = getenv("SBVR_ZT_MIN_T") ? atoi(getenv("SBVR_ZT_MIN_T")) : 12;
   if (!mma || (w->meta_kind == SBVR_META_GROUP && T >= zt_min && zt_supported(w, X)))
     return sbvr_gemv_batched(w, X, T, Y, workspace, ws_bytes, stream);
@@ -303,7 +317,7 @@ sbvr_status sbvr_gemv_to_peers(const sbvr_weights* w, const sbvr_act* X, int32_t
   s = check_act(w, X, T);
   if (s != SBVR_OK) return s;
   if (!peer_y) return set_error(SBVR_ERR_INVALID_ARG, "peer_y is NULL");
-  if (w->meta_kind == SBVR_META_INDEXED && (X->kind != SBVR_ACT_SBVR || w->K < 2 || w->K > 4))
+  if (w->meta_kind == SBVR_META_INDEXED && (X->kind == SBVR_ACT_FP16 || w->K < 2 || w->K > 4))
     return set_error(SBVR_ERR_UNSUPPORTED, "indexed weights need SBVR-x and K 2..4");
   if (n_peers < 1 || n_peers > 8) return set_error(SBVR_ERR_INVALID_ARG, "n_peers=%d outside 1..8", n_peers);
   if (y_row_offset < 0 || M_full < w->M || y_row_offset > M_full - w->M)

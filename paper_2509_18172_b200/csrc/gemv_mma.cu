@@ -130,8 +130,11 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
   p.ws_cnt = ws ? reinterpret_cast<unsigned int*>(ws) : nullptr;
   p.ws_part = ws ? reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + mma_cnt_bytes(pl)) : nullptr;
   const bool f16x = x->kind == SBVR_ACT_FP16;
-  const uint32_t* xp = f16x ? nullptr : static_cast<const uint32_t*>(x->data);
+  const bool xq = x->kind == SBVR_ACT_FP16_Q;     // fp16 x, converted to SBVR-x in the kernel prologue (T = 1)
+  const uint32_t* xp = (f16x || xq) ? nullptr : static_cast<const uint32_t*>(x->data);
   const uint16_t* xh = f16x ? static_cast<const uint16_t*>(x->data) : nullptr;
+  p.xq = xq ? static_cast<const uint16_t*>(x->data) : nullptr;
+  p.xq_groups = 0;
   const bool debug = P_debug != nullptr;
   // SBVR-x batches: tokens as MMA columns, B = z (s8), A = the plane bits themselves (u8 0/1); one pass
   // serves 8 tokens with T_t = sum_e beta_t[e] z_e read directly from the accumulator
@@ -145,8 +148,8 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
     else TT = debug ? 1 : (rem >= 4 ? 4 : (rem >= 2 ? 2 : 1));
     const int ntok = rem < TT ? rem : TT;
     p.ntok = ntok;
-    p.xplanes = f16x ? nullptr : xp + (size_t)done * pl.NG * x->l * 4;
-    p.xscales = f16x ? nullptr : x->scales + (size_t)done * pl.NG;
+    p.xplanes = (f16x || xq) ? nullptr : xp + (size_t)done * pl.NG * x->l * 4;
+    p.xscales = (f16x || xq) ? nullptr : x->scales + (size_t)done * pl.NG;
     p.xh = f16x ? xh + (size_t)done * w->N : nullptr;
     p.Y = Y ? Y + (size_t)done * w->M : nullptr;
     for (int j = 0; j < p.n_peers; ++j) p.peer_y[j] = peers->y[j] + (size_t)done * p.M_full;
@@ -159,6 +162,7 @@ sbvr_status launch_gemv_mma(const sbvr_weights* w, const sbvr_act* x, int T, flo
       p.Pw = part == 0 ? pl.C_main : pl.C_tail;
       p.qq = Us / p.Pw;
       p.rr = Us % p.Pw;
+      if (xq) p.xq_groups = p.qq + (p.rr ? 1 : 0) < pl.NG ? p.qq + (p.rr ? 1 : 0) : pl.NG;
       // balance warp ranges at tile granularity: an extra tile pair on some warps costs a whole pair
       // step at the end of a launch, a lone tile half of it (measured on the bench step: +0.7 %, the
       // big GEMVs 1.5 % faster; a pair-granular split for small problems measured no better)

@@ -82,6 +82,8 @@ struct ImmaParams {
   const uint8_t* units;     // the weights' unit records (sbvr.h)
   const float* ratio_pow;   // [n_ratio][K]
   const uint32_t* coef_table;   // SBVR_META_INDEXED: [1 + 2 n] (n, then (s16 | b16 << 16, ratio index)); else NULL
+  const uint16_t* xq;       // XQ: fp16 x [N] converted to SBVR-x (Eq. 12) in the prologue; else NULL
+  int xq_groups;            // XQ: groups converted per CTA (shared-memory rows)
   const uint32_t* xplanes;  // [T][NG][l][4] (SBVR-x)
   const uint16_t* xh;       // [T][N] fp16 x (fp16-x path)
   int ntok;                 // fp16-x: tokens in this pass (<= 8, one per MMA column)
@@ -255,6 +257,56 @@ __device__ __forceinline__ void issue_unit(uint8_t* slot, uint64_t* bar, const I
   bulk_g2s(slot + Gm::kPlaneBytes + Gm::kSbBytes + 16 * i0, u + (size_t)R * (16 * K + kMeta - 1) + r0, nt * 16, bar);
 }
 
+// Eq. 12 for the activation groups gi = first, first + stride, ... < n of this CTA (group g0 + gi mod NG) by one
+// warp, bit-identical to encode_vector_kernel (the same fp32 IEEE ops): absmax -> s_x = absmax / (2^(l-1) - 1)
+// (__fdiv_rn), z = clamp(rne(x / s_x)), l-bit two's-complement planes by ballot; word (plane j, 32-element word c)
+// -> out[32 gi + 4 j + c], s_x -> out_s[gi].  The loads of up to four groups are issued before any arithmetic,
+// so a warp pays the L2 latency once per four groups.
+__device__ __forceinline__ void xq_convert_groups(const ImmaParams& p, int g0, int NG, int first, int stride, int n,
+                                                  uint32_t* out, float* out_s) {
+  const int lane = threadIdx.x & 31;
+  const int zmax = (1 << (p.l - 1)) - 1;
+  const uint32_t lmask = (1u << p.l) - 1u;
+  for (int gb = first; gb < n; gb += 4 * stride) {
+    float v[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gi = gb + q * stride;
+      int g = g0 + gi;
+      if (g >= NG) g -= NG;
+      const uint16_t* xg = p.xq + (size_t)g * kG;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) v[q][c] = gi < n ? __half2float(__ushort_as_half(__ldg(xg + 32 * c + lane))) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int gi = gb + q * stride;
+      if (gi >= n) break;
+      float a = fmaxf(fmaxf(fabsf(v[q][0]), fabsf(v[q][1])), fmaxf(fabsf(v[q][2]), fabsf(v[q][3])));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+      const float sx = (a != 0.0f) ? __fdiv_rn(a, (float)zmax) : 0.0f;
+      uint32_t mine = 0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        int z = 0;
+        if (sx != 0.0f) {
+          z = __float2int_rn(__fdiv_rn(v[q][c], sx));
+          z = min(max(z, -zmax), zmax);
+        }
+        const uint32_t u = (uint32_t)z & lmask;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t word = __ballot_sync(0xffffffffu, (u >> j) & 1u);
+          if (lane == 4 * j + c) mine = word;
+        }
+      }
+      out[32 * gi + lane] = lane < 4 * p.l ? mine : 0u;
+      if (lane == 0) out_s[gi] = sx;
+    }
+  }
+}
+
 // L2 prefetch of the first two units warp wib of CTA c will copy in the next GEMV of a chain (same unit-record
 // layout and work split as this kernel's main launch, SBVR_META_GROUP): cp.async.bulk.prefetch.L2, no smem.
 // (scalar arguments only: taking the address of the kernel's parameter struct would move it to local memory)
@@ -284,7 +336,7 @@ static __device__ __noinline__ void prefetch_next(const uint8_t* nx_units, int n
 // F16X: the fp16-x path (north star): M_t = sum_e beta_t[e] x_e with x in fp16, on
 // mma.m16n8k16 f16 (A = plane bits as 0/1.0 pairs, B = the lane's own x values, columns = tokens);
 // TT is then the number of token columns kept (<= 8).
-template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB, bool IDX>
+template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB, bool IDX, bool XQ>
 #ifdef SBVR_MMA_MAXNREG
 __global__ void __maxnreg__(SBVR_MMA_MAXNREG) gemv_mma_kernel(ImmaParams p) {
 #else
@@ -304,6 +356,9 @@ __global__ void __launch_bounds__(kImmaWarps * 32, SBVR_MMA_CTAS_PER_SM) gemv_mm
   __shared__ int s_lb[kImmaWarps];                 // last launch-local band of each warp (-1: no tiles)
   // dynamic smem: [rings][s_part: warps x 2 (first / last band) x TT x 64]
   float* s_part = reinterpret_cast<float*>(smem + kImmaWarps * Gm::kWarpBytes);
+  // XQ: this CTA's activation groups converted in the prologue (Eq. 12): [groups][8 planes][4 words] + scales
+  uint32_t* s_xq = reinterpret_cast<uint32_t*>(s_part + kImmaWarps * 2 * TT * 64);
+  float* s_xqs = reinterpret_cast<float*>(s_xq + 32 * p.xq_groups);
   // let the next kernel in the stream get scheduled as soon as our CTAs retire
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -360,8 +415,16 @@ __global__ void __launch_bounds__(kImmaWarps * 32, SBVR_MMA_CTAS_PER_SM) gemv_mm
     s_lb[w2] = t1 > t0 ? (V0 + (t1 - 1) / NB) / NG : -1;
   }
   __syncthreads();
+  // XQ: groups g0, g0+1, ... (mod NG) of this CTA's unit range, converted by its warps (one warp per group)
+  const int xq_g0 = V0 % NG;
+  const int xq_n = min(V1 - V0, NG);
+  if constexpr (XQ) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // x is produced by the previous kernel
+    xq_convert_groups(p, xq_g0, NG, wib, kImmaWarps, xq_n, s_xq, s_xqs);
+    __syncthreads();
+  }
   if (n_mine <= 0) return;
-  asm volatile("griddepcontrol.wait;" ::: "memory");   // activations / workspace / y only from here
+  if constexpr (!XQ) asm volatile("griddepcontrol.wait;" ::: "memory");   // activations / workspace / y from here
   if (EXPM(8)) return;
 
   // lane constants (Eq. 12: alpha_j = 2^j, alpha_{l-1} = -2^(l-1); MMA columns j0 = 2c, j1 = 2c+1)
@@ -421,6 +484,10 @@ __global__ void __launch_bounds__(kImmaWarps * 32, SBVR_MMA_CTAS_PER_SM) gemv_mm
     load_xh(g);
   } else if constexpr (ZB) {
     load_xz(g);
+  } else if constexpr (XQ) {
+    const int gi = g >= xq_g0 ? g - xq_g0 : g - xq_g0 + NG;
+    Xn[0] = gq < p.l ? s_xq[32 * gi + 4 * gq + c] : 0u;
+    sxn[0] = s_xqs[gi];
   } else {
 #pragma unroll
     for (int tk = 0; tk < TT; ++tk) {
@@ -500,6 +567,10 @@ __global__ void __launch_bounds__(kImmaWarps * 32, SBVR_MMA_CTAS_PER_SM) gemv_mm
         load_xh(gp);
       } else if constexpr (ZB) {
         load_xz(gp);
+      } else if constexpr (XQ) {
+        const int gi = gp >= xq_g0 ? gp - xq_g0 : gp - xq_g0 + NG;
+        Xn[0] = gq < p.l ? s_xq[32 * gi + 4 * gq + c] : 0u;
+        sxn[0] = s_xqs[gi];
       } else {
 #pragma unroll
         for (int tk = 0; tk < TT; ++tk) {
@@ -953,16 +1024,18 @@ __global__ void __launch_bounds__(kImmaWarps * 32, SBVR_MMA_CTAS_PER_SM) gemv_mm
 #endif
 }
 
-template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB = false, bool IDX = false>
+template <int K, int NB, int TT, bool DEBUG, bool F16X, bool ZB = false, bool IDX = false, bool XQ = false>
 inline cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
-  const int smem = kImmaWarps * Geom<K, NB, IDX>::kWarpBytes + kImmaWarps * 2 * TT * 64 * 4;
-  static bool attr[64] = {false};     // the attribute is per device
+  const int smem = kImmaWarps * Geom<K, NB, IDX>::kWarpBytes + kImmaWarps * 2 * TT * 64 * 4 +
+                   (XQ ? p.xq_groups * (32 * 4 + 4) : 0);
+  // the attribute is per device; XQ's shared memory grows with the groups per CTA, so keep the largest set
+  static int attr_smem[64] = {0};
   const int dev = cur_device();
-  if (dev < 0 || dev >= 64 || !attr[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB, IDX>,
+  if (dev < 0 || dev >= 64 || attr_smem[dev] < smem) {
+    cudaError_t e = cudaFuncSetAttribute(gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB, IDX, XQ>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    if (dev >= 0 && dev < 64) attr[dev] = true;
+    if (dev >= 0 && dev < 64) attr_smem[dev] = smem;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.Pw);
@@ -977,11 +1050,18 @@ inline cudaError_t launch_one(const ImmaParams& p, cudaStream_t st) {
   attr_pdl[1].val.cooperative = coop;
   cfg.attrs = attr_pdl;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB, IDX>, p);
+  return cudaLaunchKernelEx(&cfg, gemv_mma_kernel<K, NB, TT, DEBUG, F16X, ZB, IDX, XQ>, p);
 }
 
 template <int K, int NB>
 inline cudaError_t launch_nb(const ImmaParams& p, int TT, bool debug, bool f16x, bool zb, cudaStream_t st) {
+  if (p.xq) {                              // fp16 x converted in the prologue: batch 1, SBVR-x form, K 2..4
+    if constexpr (K >= 2 && K <= 4) {
+      if (p.coef_table) return launch_one<K, NB, 1, false, false, false, true, true>(p, st);
+      return launch_one<K, NB, 1, false, false, false, false, true>(p, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (p.coef_table) {                      // SBVR_META_INDEXED weights: SBVR-x forms, K 2..4 (checked by the ABI)
     if constexpr (K >= 2 && K <= 4) {
       if (zb) return launch_one<K, NB, 8, false, false, true, true>(p, st);

@@ -3,6 +3,7 @@ SBVR_LIB_AB=ab/libsbvr_diag.so -- the production kernel has no timestamp code.)
 Per-warp timestamps of the batch-1 MMA GEMV inside a CUDA-graph chain (env SBVR_TS_PTR):
 0 warp start, 1 first unit landed, 2 last unit computed, 3 exit (after band hand-off).
 Graph of 20 launches over distinct weight copies; stamps of the 10th launch (warm, PDL-overlapped).
+--xq: fp16 x converted in the GEMV prologue (SBVR_ACT_FP16_Q; stamp 1 then includes the conversion).
 Prints percentiles over warps in us relative to the earliest start of that launch."""
 import json
 import os
@@ -21,7 +22,7 @@ for name, M, N in [("k_proj", 1024, 4096), ("q_proj", 4096, 4096), ("gate_proj",
     ring = max(2, int(4 * 132e6 // (M * N // 2)) + 1)
     ws = [sb.pack_canonical(pc, s16, b16, ri, 16) for _ in range(min(ring, 20))]
     x = torch.from_numpy(synthetic.activation(N, seed=6)).cuda()
-    act = sb.encode_vector(x)
+    act = sb.fp16q_activation(x[0]) if "--xq" in sys.argv else sb.encode_vector(x)
     wsp = sb.Workspace.for_weights(ws[0], 1)
     y = torch.empty(1, M, device="cuda")
     st = torch.cuda.Stream()
