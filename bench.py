@@ -592,10 +592,13 @@ def layer_chain(sb, device, reps=20):
     converting its own input (sbvr_encode_vector + sbvr_gemv for q, k, v, o, gate, up, down -- unfused,
     7 + 7 launches), one CUDA graph over a ring of layers (> L2), device time per layer (the TPOT-like
     per-layer GEMV latency of Table 3's setting).  Also the fused form (qkv and gate_up stacked,
-    4 conversions) for comparison."""
+    4 conversions) for comparison, and both with the conversion done in each GEMV's prologue (SBVR_ACT_FP16_Q:
+    7 / 4 launches, bit-identical y)."""
     out = {}
-    for label, mats in (("unfused_7", [(n, M, N) for n, M, N in synthetic.LLAMA3_8B_LAYER]),
-                        ("fused_4", [(n, M, N) for n, M, N, _, _ in FUSED])):
+    unf = [(n, M, N) for n, M, N in synthetic.LLAMA3_8B_LAYER]
+    fus = [(n, M, N) for n, M, N, _, _ in FUSED]
+    for label, mats, xq in (("unfused_7", unf, False), ("fused_4", fus, False),
+                            ("unfused_7_in_kernel_conversion", unf, True), ("fused_4_in_kernel_conversion", fus, True)):
         ring = 3
         layers = []
         for r in range(ring):
@@ -606,12 +609,13 @@ def layer_chain(sb, device, reps=20):
                 ws_.append((w, sb.Workspace.for_weights(w, 1), torch.empty(M, device=device),
                             torch.from_numpy(synthetic.activation(N, seed=i)).to(device)))
             layers.append(ws_)
-        acts = [[sb.encode_vector(x) for (_, _, _, x) in L] for L in layers]
+        acts = [[sb.fp16q_activation(x[0]) if xq else sb.encode_vector(x) for (_, _, _, x) in L] for L in layers]
         stream = torch.cuda.Stream(device)
         with torch.cuda.stream(stream):
             def one(r):
                 for (w, wsp, y, x), a in zip(layers[r], acts[r]):
-                    sb.encode_vector(x, out=a)
+                    if not xq:
+                        sb.encode_vector(x, out=a)
                     sb.gemv(w, a, y=y, ws=wsp)
             for r in range(ring):
                 one(r)
@@ -628,7 +632,7 @@ def layer_chain(sb, device, reps=20):
             torch.cuda.synchronize()
         us = a.elapsed_time(b) * 1e3 / reps
         byts = sum(sb.algorithmic_bytes(M, N, K_BITS, act="sbvr", l=L_BITS, T=1) for (_, M, N) in mats)
-        out[label] = {"us_per_layer": round(us, 2), "launches_per_layer": 2 * len(mats),
+        out[label] = {"us_per_layer": round(us, 2), "launches_per_layer": (1 if xq else 2) * len(mats),
                       "GBps": round(byts / (us * 1e-6) / 1e9, 1),
                       "x32_layers_ms": round(32 * us / 1e3, 3)}
         del layers, acts

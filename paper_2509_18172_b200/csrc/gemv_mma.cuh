@@ -73,6 +73,12 @@ constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at leas
 #define SBVR_MMA_SLOTS 2
 #endif
 constexpr int kSlots = SBVR_MMA_SLOTS;   // shared-memory ring depth per warp
+// weight copies a warp issues at launch; the rest of the ring is filled when the first unit lands (a smaller
+// initial burst lets the first units arrive sooner, so compute overlaps the stream)
+#ifndef SBVR_MMA_INIT_SLOTS
+#define SBVR_MMA_INIT_SLOTS SBVR_MMA_SLOTS
+#endif
+constexpr int kInitSlots = SBVR_MMA_INIT_SLOTS;
 constexpr int kMaxTT = 4;            // tokens per pass (batched)
 constexpr int kZbMinT = 3;           // SBVR-x batches from this T use the z-column formulation (8 tokens per pass)
 constexpr int kSumBatchMax = 8;      // CTA partials loaded per batch by a band's owner (x TT words per lane)
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(kImmaWarps * 32, SBVR_MMA_CTAS_PER_SM) gemv_mm
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 #pragma unroll
     for (int s2 = 0; s2 < kSlots; ++s2)
-      if (s2 < n_mine && !EXPM(2)) issue_next(ring + s2 * Gm::kSlotBytes, bars + s2, s2);
+      if (s2 < kInitSlots && s2 < n_mine && !EXPM(2)) issue_next(ring + s2 * Gm::kSlotBytes, bars + s2, s2);
   }
   for (int i = threadIdx.x; i < p.n_ratio; i += blockDim.x) s_rat[i] = K >= 2 ? p.ratio_pow[i * K + 1] : 0.f;
   if constexpr (IDX)      // entry e -> (fp16 s | b << 16, r as fp32 bits): one 8-byte shared load per row and tile
@@ -583,6 +589,10 @@ __global__ void __launch_bounds__(kImmaWarps * 32, SBVR_MMA_CTAS_PER_SM) gemv_mm
     uint8_t* sl = ring + slot * Gm::kSlotBytes;
     if (!EXPM(2)) mbar_wait(bars + slot, phase);
     if (k == 0) TSW(1);
+    if constexpr (kInitSlots < kSlots) {     // deferred part of the initial fill (in unit order)
+      if (k == 0 && lane == 0 && !EXPM(2))
+        for (int s2 = kInitSlots; s2 < kSlots && s2 < n_mine; ++s2) issue_next(ring + s2 * Gm::kSlotBytes, bars + s2, s2);
+    }
 
     // tiles are processed two at a time (PT = 2: 4K independent MMA chains hide the IMMA latency); a
     // warp range that starts or ends inside a pair takes that tile alone (PT = 1)
