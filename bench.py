@@ -265,6 +265,13 @@ def run_sbvr(args, world, rank, local_rank, pg):
             symm = [[sdist.SymmRowShardedGemv(w, M, 1, pg, ws) for (_, M, N, r0, r1, w, ws, xin) in mats]
                     for mats in layers]
         y_host = [torch.zeros(M, dtype=torch.float32).pin_memory() for (_, M, N, _, _) in FUSED]
+        # grouped step: the layer set's 4 GEMVs (independent problems over the converted inputs) in ONE persistent
+        # sbvr_gemv_group launch; one workspace per ring layer
+        group_probs = group_ws = None
+        if args.step == "group":
+            group_probs = [[(w, acts[xin], ys[r][j]) for j, (name, M, N, r0, r1, w, ws, xin) in enumerate(layers[r])]
+                           for r in range(ring)]
+            group_ws = [sb.group_workspace(p) for p in group_probs]
     torch.cuda.synchronize()
 
     def step(r, events=None, span=None, e2e=False):
@@ -275,7 +282,16 @@ def run_sbvr(args, world, rank, local_rank, pg):
             sb.encode_vector(xs[0], out=act_all)
         if span is not None:
             cr.record_external(span[0], stream)
-        for j, (name, M, N, r0, r1, w, ws, xin) in enumerate(layers[r]):
+        if group_probs is not None:
+            if events is not None:
+                cr.record_external(events[0][0], stream)
+            sb.gemv_group(group_probs[r], ws=group_ws[r])
+            if events is not None:
+                cr.record_external(events[0][1], stream)
+            if world > 1:
+                for j in range(len(layers[r])):
+                    sdist.all_gather_rows_into(yfull[j], ys[r][j], group=pg)
+        for j, (name, M, N, r0, r1, w, ws, xin) in enumerate(layers[r] if group_probs is None else []):
             if events is not None:
                 cr.record_external(events[j][0], stream)
             if symm is not None:                        # all-gather fused into the GEMV epilogue (dist.py)
@@ -426,7 +442,8 @@ def run_sbvr(args, world, rank, local_rank, pg):
             g, gevs = split_graphs[i % ring]
             g.replay()
             torch.cuda.synchronize()
-            per_gemv_ms += [cr.elapsed_ms(a, b) for a, b in gevs]
+            per_gemv_ms += [cr.elapsed_ms(a, b) if (group_probs is None or k == 0) else 0.0
+                            for k, (a, b) in enumerate(gevs)]
     gemv_ms_avg = per_gemv_ms / n_split
     res = dict(elapsed=elapsed, e2e_ms=e2e_ms, step_bytes=step_bytes, step_gemv_bytes=step_gemv_bytes,
                gemv_ms_avg=gemv_ms_avg, rank_gemv_bytes=rank_gemv_bytes, clocks=clocks,
@@ -747,6 +764,10 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+# ncu dram bytes per launch of the step's GEMV launches (tools/traffic_from_ncu.py)
+TRAFFIC_FILE = {"chain": "r02_ncu_traffic.json", "group": "r02_ncu_traffic_group.json"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -760,6 +781,9 @@ def main():
     ap.add_argument("--chain", action="store_true",
                     help="launch the step's GEMVs with sbvr_gemv_chain (L2 prefetch of the next GEMV's first units; "
                          "measured no gain: profiles/r02_chain_ab.txt)")
+    ap.add_argument("--step", default="group", choices=["group", "chain"],
+                    help="group: the layer set's 4 GEMVs in one persistent sbvr_gemv_group launch (default); chain: "
+                         "4 sbvr_gemv launches chained by programmatic dependent launch")
     ap.add_argument("--allgather", default="nccl", choices=["nccl", "symm"],
                     help="N > 1: join y with an NCCL all-gather, or store it to every rank from the GEMV epilogue "
                          "(symmetric memory, dist.SymmRowShardedGemv)")
@@ -768,6 +792,8 @@ def main():
     ap.add_argument("--no-encode", action="store_true")
     ap.add_argument("--no-sweeps", action="store_true")
     args = ap.parse_args()
+    if args.allgather == "symm" or args.fused_conversion or args.chain:
+        args.step = "chain"                        # those variants exist on the per-GEMV launches only
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
@@ -819,21 +845,27 @@ def main():
     gemv_ms = res["gemv_ms_avg"]
     shapes = layer_shapes()
     per = []
-    for j, (name, M, N, xin, members) in enumerate(FUSED):
+    group = args.step == "group"
+    for j, (name, M, N, xin, members) in enumerate(FUSED if not group else []):
         b = res["rank_gemv_bytes"][j]
         per.append({"gemv": name, "projections": list(members), "M": M, "N": N, "rows_per_rank": M // world,
                     "us_serialized": round(gemv_ms[j] * 1e3, 3), "GBps": round(b / (gemv_ms[j] * 1e-3) / 1e9, 1)})
+    if group:
+        b = sum(res["rank_gemv_bytes"])
+        per.append({"gemv": "group(" + ",".join(f[0] for f in FUSED) + ")", "us_serialized": round(gemv_ms[0] * 1e3, 3),
+                    "GBps": round(b / (gemv_ms[0] * 1e-3) / 1e9, 1)})
+    n_launch_gemv = 1 if group else len(FUSED)
     tot_b = sum(res["rank_gemv_bytes"])
     achieved = tot_b / (res["span_ms_avg"] * 1e-3) / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    tp = os.path.join(ROOT, "profiles", TRAFFIC_FILE[args.step])
     if os.path.exists(tp):
         try:
             traffic = json.load(open(tp)).get("traffic_bytes_per_launch_mean")
         except Exception:
             traffic = None
     e2e_val = res["step_bytes"] / (res["e2e_ms"] / K * 1e-3) / 1e9
-    launches = K * ((0 if args.fused_conversion else 1) + len(FUSED))
+    launches = K * ((0 if args.fused_conversion else 1) + n_launch_gemv)
     sm = np.asarray(res["step_ms"]) * 1e3
     step_stats = {"us_median": round(float(np.median(sm)), 3), "us_p10": round(float(np.percentile(sm, 10)), 3),
                   "us_p90": round(float(np.percentile(sm, 90)), 3), "us_mean": round(float(sm.mean()), 3)}
@@ -871,18 +903,24 @@ def main():
                                                                        " + y stored to every rank by the GEMV epilogue "
                                                                        "(symmetric memory) + signal-pad barrier")
                                                                       if world > 1 else ""),
-                   "path": "sbvr_encode_vector x1 (the 4 layer inputs) + sbvr_gemv x4 (fused qkv, o, fused gate_up, down; "
-                           "bit-sliced AND/popcount on the int8 tensor pipe, mma.sync m16n8k32 u8, kernel gemv_mma), "
-                           "one CUDA graph per step, programmatic dependent launch"},
+                   "path": ("sbvr_encode_vector x1 (the 4 layer inputs) + sbvr_gemv_group x1 over the layer set (fused "
+                            "qkv, o, fused gate_up, down as 4 independent problems of one persistent launch; bit-sliced "
+                            "AND/popcount on the int8 tensor pipe, mma.sync m16n8k32 u8, kernel gemv_group), one CUDA "
+                            "graph per step, programmatic dependent launch" if group else
+                            "sbvr_encode_vector x1 (the 4 layer inputs) + sbvr_gemv x4 (fused qkv, o, fused gate_up, "
+                            "down; bit-sliced AND/popcount on the int8 tensor pipe, mma.sync m16n8k32 u8, kernel "
+                            "gemv_mma), one CUDA graph per step, programmatic dependent launch"),
+                   "step": args.step},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "gemv_mma_kernel<4,4,1,false> (the 4 GEMV launches of a step)",
-                     "how": "algorithmic bytes per launch / average launch duration over the 4 back-to-back GEMV "
-                            "launches of a step (= their summed bytes / the CUDA-event span around them; external "
-                            f"event nodes in {res['span_n']} of the {K} timed steps, every {EV_EVERY}th); traffic "
-                            "= ncu dram read+write bytes per launch, same 4 launches (profiles/r02_ncu_traffic.json)",
+                     "kernel": ("gemv_group_kernel<4> (the step's one grouped GEMV launch)" if group else
+                                "gemv_mma_kernel<4,4,1,false,false,false,false,false> (the 4 GEMV launches of a step)"),
+                     "how": "algorithmic bytes per launch / average launch duration over the step's GEMV launches "
+                            "(= their summed bytes / the CUDA-event span around them; external event nodes in "
+                            f"{res['span_n']} of the {K} timed steps, every {EV_EVERY}th); traffic = ncu dram "
+                            "read+write bytes per launch (profiles/" + TRAFFIC_FILE[args.step] + ")",
                      "gemv_span_us": round(res["span_ms_avg"] * 1e3, 3),
-                     "algorithmic_bytes_per_launch": round(tot_b / len(FUSED))},
+                     "algorithmic_bytes_per_launch": round(tot_b / n_launch_gemv)},
         "per_gemv": per,
         "per_gemv_how": "diagnostic after the timed region: event nodes between the 4 launches (no launch "
                         "overlap), so each figure includes a full launch + ramp",

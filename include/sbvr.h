@@ -238,6 +238,28 @@ sbvr_status sbvr_gemv_to_peers(const sbvr_weights* w, const sbvr_act* X, int32_t
                                int32_t n_peers, int32_t y_row_offset, int32_t M_full, void* workspace, size_t ws_bytes,
                                void* stream);
 
+/* sbvr_gemv_group -- several INDEPENDENT batch-1 GEMVs y_p = W_p x_p (the SBVR-x AND+popcount form of
+ * sbvr_gemv) in one persistent launch, e.g. the projections of a decoder layer whose inputs are all available
+ * (grouped GEMV).  The problems' unit records form one work sequence that is split evenly over the CTAs, so the
+ * fixed costs of a launch (pipeline fill, split-K combine, tail, launch boundary) are paid once per group instead
+ * of once per matrix, and the next matrix's weights stream in while the current one finishes.
+ *   probs: HOST array of n (1..SBVR_GROUP_MAX) problems; each holds a weights and an activation descriptor (by
+ *          value) and y (device fp32 [M]).  No problem may write a buffer another problem reads (y's must not
+ *          overlap x, scales or weights); y's must not overlap each other.
+ *   Supported: SBVR_ACT_SBVR activations (T = 1, the same l for all), SBVR_META_GROUP weights, K in 2..4 and equal
+ *   for all problems, M % 128 == 0 (SBVR_ERR_UNSUPPORTED / SBVR_ERR_SHAPE otherwise).
+ *   workspace: >= sbvr_gemv_group_workspace_bytes bytes, initialised once with sbvr_workspace_init and left at
+ *   rest by every call; not shared with a concurrently running GEMV.
+ * Arithmetic and per-band reduction order are those of sbvr_gemv's MMA kernel; y is deterministic. */
+#define SBVR_GROUP_MAX 8
+typedef struct {
+  sbvr_weights w;
+  sbvr_act x;
+  float* y;
+} sbvr_gemv_problem;
+sbvr_status sbvr_gemv_group_workspace_bytes(const sbvr_gemv_problem* probs, int32_t n, size_t* bytes);
+sbvr_status sbvr_gemv_group(const sbvr_gemv_problem* probs, int32_t n, void* workspace, size_t ws_bytes, void* stream);
+
 /* sbvr_gemv_ex -- as sbvr_gemv_batched with an explicit algorithm (sbvr_algo). */
 sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
                          size_t ws_bytes, int32_t algo, void* stream);

@@ -94,6 +94,9 @@ def lib():
                 getattr(L, name).argtypes = at
         if hasattr(L, "sbvr_gemv_chain"):
             L.sbvr_gemv_chain.argtypes = [P, P, i32, P, P, sz, P, P]
+        if hasattr(L, "sbvr_gemv_group"):
+            L.sbvr_gemv_group.argtypes = [P, i32, P, sz, P]
+            L.sbvr_gemv_group_workspace_bytes.argtypes = [P, i32, P]
         if hasattr(L, "sbvr_gemv_to_peers"):
             L.sbvr_gemv_to_peers.argtypes = [P, P, i32, P, i32, i32, i32, P, sz, P]
         # (A/B timing loads older builds through SBVR_LIB_AB: symbols they lack are simply not declared)
@@ -101,7 +104,8 @@ def lib():
                      "sbvr_workspace_init", "sbvr_gemv", "sbvr_gemv_batched", "sbvr_gemv_ex", "sbvr_debug_partials",
                      "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows", "sbvr_encode_weights_cached",
                      "sbvr_debug_zt_sums", "sbvr_gemv_to_peers", "sbvr_weights_bytes_ex",
-                     "sbvr_encode_weights_indexed", "sbvr_pack_indexed", "sbvr_unpack_indexed", "sbvr_gemv_chain"):
+                     "sbvr_encode_weights_indexed", "sbvr_pack_indexed", "sbvr_unpack_indexed", "sbvr_gemv_chain",
+                     "sbvr_gemv_group", "sbvr_gemv_group_workspace_bytes"):
             if hasattr(L, name):
                 getattr(L, name).restype = i32
         _lib = L
@@ -395,6 +399,42 @@ def gemv_to_peers(w: SbvrWeights, x: SbvrActivation, peer_ptrs, y_row_offset: in
     wd, xd = w.desc(), x.desc()
     _check(lib().sbvr_gemv_to_peers(ctypes.byref(wd), ctypes.byref(xd), x.T, arr, len(peer_ptrs), int(y_row_offset),
                                     int(M_full), _ptr(ws.buf), ws.nbytes, _stream()), "sbvr_gemv_to_peers")
+
+
+GROUP_MAX = 8
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [("w", _Weights), ("x", _Act), ("y", ctypes.c_void_p)]
+
+
+def _problems(problems):
+    arr = (_Problem * len(problems))()
+    for i, (w, x, y) in enumerate(problems):
+        arr[i].w = w.desc()
+        arr[i].x = x.desc()
+        arr[i].y = y.data_ptr() if y is not None else 0
+    return arr
+
+
+def group_workspace(problems) -> Workspace:
+    """Workspace for sbvr_gemv_group over `problems` [(w, x, y), ...] (y may be None here)."""
+    n = ctypes.c_size_t()
+    arr = _problems(problems)
+    _check(lib().sbvr_gemv_group_workspace_bytes(arr, len(problems), ctypes.byref(n)), "sbvr_gemv_group_workspace_bytes")
+    return Workspace(n.value, problems[0][0].data.device)
+
+
+def gemv_group(problems, ws: Optional[Workspace] = None):
+    """sbvr_gemv_group: independent batch-1 SBVR-x GEMVs y_p = W_p x_p in one persistent launch.
+    problems: [(w, x, y or None), ...]; returns the list of y tensors."""
+    problems = [(w, x, y if y is not None else torch.empty(w.M, dtype=torch.float32, device=w.data.device))
+                for (w, x, y) in problems]
+    if ws is None:
+        ws = group_workspace(problems)
+    arr = _problems(problems)
+    _check(lib().sbvr_gemv_group(arr, len(problems), _ptr(ws.buf), ws.nbytes, _stream()), "sbvr_gemv_group")
+    return [y for (_, _, y) in problems]
 
 
 def debug_partials(w: SbvrWeights, x: SbvrActivation, algo: int = ALGO_TC) -> torch.Tensor:

@@ -336,6 +336,44 @@ sbvr_status sbvr_gemv_to_peers(const sbvr_weights* w, const sbvr_act* X, int32_t
   return launch_gemv_mma(w, X, T, nullptr, workspace, ws_bytes, nullptr, (cudaStream_t)stream, &po);
 }
 
+static sbvr_status check_group(const sbvr_gemv_problem* probs, int32_t n) {
+  if (!probs) return set_error(SBVR_ERR_INVALID_ARG, "probs is NULL");
+  if (n < 1 || n > SBVR_GROUP_MAX) return set_error(SBVR_ERR_INVALID_ARG, "n=%d outside 1..%d", n, SBVR_GROUP_MAX);
+  for (int i = 0; i < n; ++i) {
+    const sbvr_gemv_problem& p = probs[i];
+    sbvr_status s = check_weights(&p.w);
+    if (s != SBVR_OK) return s;
+    s = check_act(&p.w, &p.x, 1);
+    if (s != SBVR_OK) return s;
+    if (!p.y) return set_error(SBVR_ERR_INVALID_ARG, "problem %d: y is NULL", i);
+    if (p.x.kind != SBVR_ACT_SBVR) return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: grouped GEMV needs SBVR-x", i);
+    if (p.w.meta_kind != SBVR_META_GROUP)
+      return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: grouped GEMV needs SBVR_META_GROUP weights", i);
+    if (p.w.K < 2 || p.w.K > 4) return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: K=%d outside 2..4", i, p.w.K);
+    if (p.w.K != probs[0].w.K) return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: K differs from problem 0", i);
+    if (p.x.l != probs[0].x.l) return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: l differs from problem 0", i);
+    if (p.w.M % kRowBlock) return set_error(SBVR_ERR_SHAPE, "problem %d: M=%d not a multiple of 128", i, p.w.M);
+  }
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_gemv_group_workspace_bytes(const sbvr_gemv_problem* probs, int32_t n, size_t* bytes) {
+  if (!bytes) return set_error(SBVR_ERR_INVALID_ARG, "bytes is NULL");
+  if (!probs || n < 1 || n > SBVR_GROUP_MAX) return set_error(SBVR_ERR_INVALID_ARG, "probs/n invalid");
+  for (int i = 0; i < n; ++i)
+    if (probs[i].w.M <= 0 || probs[i].w.N <= 0 || probs[i].w.M % kRowBlock || probs[i].w.N % kG)
+      return set_error(SBVR_ERR_SHAPE, "problem %d: bad M/N %d/%d", i, probs[i].w.M, probs[i].w.N);
+  *bytes = group_workspace_bytes(probs, n);
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_gemv_group(const sbvr_gemv_problem* probs, int32_t n, void* workspace, size_t ws_bytes, void* stream) {
+  sbvr_status s = check_group(probs, n);
+  if (s != SBVR_OK) return s;
+  if (!workspace) return set_error(SBVR_ERR_WORKSPACE, "workspace is NULL");
+  return launch_gemv_group(probs, n, workspace, ws_bytes, (cudaStream_t)stream);
+}
+
 sbvr_status sbvr_gemv_batched(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
                               size_t ws_bytes, void* stream) {
   return sbvr_gemv_ex(w, X, T, Y, workspace, ws_bytes, SBVR_ALGO_AUTO, stream);
