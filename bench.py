@@ -269,7 +269,13 @@ def run_sbvr(args, world, rank, local_rank, pg):
         # sbvr_gemv_group launch; one workspace per ring layer
         group_probs = group_ws = None
         if args.step == "group":
-            group_probs = [[(w, acts[xin], ys[r][j]) for j, (name, M, N, r0, r1, w, ws, xin) in enumerate(layers[r])]
+            gacts = acts
+            if args.xconv == "kernel":                 # the grouped kernel converts the fp16 inputs (Eq. 12) itself
+                gacts, e0 = [], 0
+                for n in INPUT_N:
+                    gacts.append(sb.fp16q_activation(xs[0][e0:e0 + n], l=L_BITS))
+                    e0 += n
+            group_probs = [[(w, gacts[xin], ys[r][j]) for j, (name, M, N, r0, r1, w, ws, xin) in enumerate(layers[r])]
                            for r in range(ring)]
             group_ws = [sb.group_workspace(p) for p in group_probs]
     torch.cuda.synchronize()
@@ -278,7 +284,7 @@ def run_sbvr(args, world, rank, local_rank, pg):
         if e2e:
             for x, xh in zip(xs, xs_host):
                 x.copy_(xh, non_blocking=True)
-        if not args.fused_conversion:
+        if not args.fused_conversion and not (group_probs is not None and args.xconv == "kernel"):
             sb.encode_vector(xs[0], out=act_all)
         if span is not None:
             cr.record_external(span[0], stream)
@@ -383,6 +389,7 @@ def run_sbvr(args, world, rank, local_rank, pg):
 
         # --- timed region: exactly K steps, barrier + sync on both sides; an event after every step
         span_ms, span_n = 0.0, 0
+        ev_every = min(EV_EVERY, max(1, args.steps // 4))   # short runs (--steps 20) still get span samples
         pending = {}
         if world > 1:
             torch.distributed.barrier(group=pg)
@@ -391,8 +398,8 @@ def run_sbvr(args, world, rank, local_rank, pg):
         wall0 = time.time()
         evs[0].record(stream)
         for s in range(args.steps):
-            if s % EV_EVERY == EV_EVERY - 1:
-                gi = s % ring + ring * ((s // EV_EVERY) % 2)   # same layer as a plain step s: ring order kept
+            if s % ev_every == ev_every - 1:
+                gi = s % ring + ring * ((s // ev_every) % 2)   # same layer as a plain step s: ring order kept
                 if gi in pending:                  # read the previous replay of this graph before reusing its events
                     span_ms += cr.elapsed_ms(*ev_graphs[gi][1])
                     span_n += 1
@@ -447,7 +454,7 @@ def run_sbvr(args, world, rank, local_rank, pg):
     gemv_ms_avg = per_gemv_ms / n_split
     res = dict(elapsed=elapsed, e2e_ms=e2e_ms, step_bytes=step_bytes, step_gemv_bytes=step_gemv_bytes,
                gemv_ms_avg=gemv_ms_avg, rank_gemv_bytes=rank_gemv_bytes, clocks=clocks,
-               span_ms_avg=span_ms / max(span_n, 1), span_n=span_n, step_ms=step_ms)
+               span_ms_avg=span_ms / max(span_n, 1), span_n=span_n, step_ms=step_ms, ev_every=ev_every)
     h2d = sum(x.numel() * 2 for x in xs_host)
     d2h = sum(y.numel() * 4 for y in y_host)
     res["h2d"], res["d2h"] = h2d, d2h
@@ -784,6 +791,9 @@ def main():
     ap.add_argument("--step", default="group", choices=["group", "chain"],
                     help="group: the layer set's 4 GEMVs in one persistent sbvr_gemv_group launch (default); chain: "
                          "4 sbvr_gemv launches chained by programmatic dependent launch")
+    ap.add_argument("--xconv", default="launch", choices=["kernel", "launch"],
+                    help="group step: one sbvr_encode_vector launch precedes the grouped GEMV (default), or the grouped kernel converts the fp16 layer inputs itself (Eq. 12, bit-identical; "
+                         "measured ~3.5 us slower per step: the first read of the freshly converted planes is slow)")
     ap.add_argument("--allgather", default="nccl", choices=["nccl", "symm"],
                     help="N > 1: join y with an NCCL all-gather, or store it to every rank from the GEMV epilogue "
                          "(symmetric memory, dist.SymmRowShardedGemv)")
@@ -865,7 +875,8 @@ def main():
         except Exception:
             traffic = None
     e2e_val = res["step_bytes"] / (res["e2e_ms"] / K * 1e-3) / 1e9
-    launches = K * ((0 if args.fused_conversion else 1) + n_launch_gemv)
+    conv_launch = 0 if (args.fused_conversion or (group and args.xconv == "kernel")) else 1
+    launches = K * (conv_launch + n_launch_gemv)
     sm = np.asarray(res["step_ms"]) * 1e3
     step_stats = {"us_median": round(float(np.median(sm)), 3), "us_p10": round(float(np.percentile(sm, 10)), 3),
                   "us_p90": round(float(np.percentile(sm, 90)), 3), "us_mean": round(float(sm.mean()), 3)}
@@ -903,21 +914,24 @@ def main():
                                                                        " + y stored to every rank by the GEMV epilogue "
                                                                        "(symmetric memory) + signal-pad barrier")
                                                                       if world > 1 else ""),
-                   "path": ("sbvr_encode_vector x1 (the 4 layer inputs) + sbvr_gemv_group x1 over the layer set (fused "
-                            "qkv, o, fused gate_up, down as 4 independent problems of one persistent launch; bit-sliced "
+                   "path": (("sbvr_encode_vector x1 (the 4 layer inputs) + " if args.xconv == "launch" else "") +
+                            "sbvr_gemv_group x1 over the layer set (fused qkv, o, fused gate_up, down as 4 independent "
+                            "problems of one persistent launch" + ("" if args.xconv == "launch" else ", whose prologue "
+                            "converts the 4 fp16 inputs to SBVR-x, Eq. 12") + "; bit-sliced "
                             "AND/popcount on the int8 tensor pipe, mma.sync m16n8k32 u8, kernel gemv_group), one CUDA "
                             "graph per step, programmatic dependent launch" if group else
                             "sbvr_encode_vector x1 (the 4 layer inputs) + sbvr_gemv x4 (fused qkv, o, fused gate_up, "
                             "down; bit-sliced AND/popcount on the int8 tensor pipe, mma.sync m16n8k32 u8, kernel "
                             "gemv_mma), one CUDA graph per step, programmatic dependent launch"),
-                   "step": args.step},
+                   "step": args.step, "x_conversion": ("in the GEMV kernel" if (args.fused_conversion or (
+                       group and args.xconv == "kernel")) else "sbvr_encode_vector launch")},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "kernel": ("gemv_group_kernel<4> (the step's one grouped GEMV launch)" if group else
                                 "gemv_mma_kernel<4,4,1,false,false,false,false,false> (the 4 GEMV launches of a step)"),
                      "how": "algorithmic bytes per launch / average launch duration over the step's GEMV launches "
                             "(= their summed bytes / the CUDA-event span around them; external event nodes in "
-                            f"{res['span_n']} of the {K} timed steps, every {EV_EVERY}th); traffic = ncu dram "
+                            f"{res['span_n']} of the {K} timed steps, every {res['ev_every']}th); traffic = ncu dram "
                             "read+write bytes per launch (profiles/" + TRAFFIC_FILE[args.step] + ")",
                      "gemv_span_us": round(res["span_ms_avg"] * 1e3, 3),
                      "algorithmic_bytes_per_launch": round(tot_b / n_launch_gemv)},

@@ -346,7 +346,10 @@ static sbvr_status check_group(const sbvr_gemv_problem* probs, int32_t n) {
     s = check_act(&p.w, &p.x, 1);
     if (s != SBVR_OK) return s;
     if (!p.y) return set_error(SBVR_ERR_INVALID_ARG, "problem %d: y is NULL", i);
-    if (p.x.kind != SBVR_ACT_SBVR) return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: grouped GEMV needs SBVR-x", i);
+    if (p.x.kind != SBVR_ACT_SBVR && p.x.kind != SBVR_ACT_FP16_Q)
+      return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: grouped GEMV needs SBVR-x or SBVR_ACT_FP16_Q", i);
+    if (p.x.kind != probs[0].x.kind)
+      return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: activation kind differs from problem 0", i);
     if (p.w.meta_kind != SBVR_META_GROUP)
       return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: grouped GEMV needs SBVR_META_GROUP weights", i);
     if (p.w.K < 2 || p.w.K > 4) return set_error(SBVR_ERR_UNSUPPORTED, "problem %d: K=%d outside 2..4", i, p.w.K);

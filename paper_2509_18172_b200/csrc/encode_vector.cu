@@ -13,9 +13,12 @@ namespace sbvr {
 __global__ void __launch_bounds__(256) encode_vector_kernel(const uint16_t* __restrict__ x, int total_groups, int l,
                                                             uint32_t* __restrict__ planes,
                                                             float* __restrict__ scales) {
-  // programmatic dependent launch: the planes we write may still be read by the previous GEMV
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // programmatic dependent launch: let the next kernel (the GEMV that reads our planes) be scheduled at once -- its
+  // CTAs take SMs as the previous GEMV's CTAs retire and start streaming their weights, which do not depend on us;
+  // its griddepcontrol.wait still waits for this grid to complete.  We wait for the previous kernel before writing:
+  // it may still be reading the planes we overwrite.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // group index over [T][N/G]
   if (q >= total_groups) return;

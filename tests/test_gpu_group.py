@@ -48,8 +48,11 @@ class _CanaryWs:
         self.nbytes = n
         self.buf.fill_(0xFF)
 
+    def canary_ok(self):
+        return bool(torch.all(self.full[self.nbytes:] == 0x5A))
+
     def ok(self):
-        return bool(torch.all(self.full[self.nbytes:] == 0x5A)) and bool(torch.all(self.buf == 0xFF))
+        return self.canary_ok() and bool(torch.all(self.buf == 0xFF))
 
 
 @pytest.mark.parametrize("K", [2, 3, 4])
@@ -179,3 +182,32 @@ def test_group_rejections():
     with pytest.raises(sb.SbvrError) as e:
         sb.gemv_group([(w, act, y)] * 9)
     assert e.value.status == sb.ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("l", [8, 4])
+def test_group_in_kernel_conversion_bit_identical(l):
+    """SBVR_ACT_FP16_Q problems: the kernel converts every problem's fp16 x itself (Eq. 12, distributed over the
+    grid, then a grid-wide arrival count) -- y bit-identical to sbvr_encode_vector + the grouped GEMV on SBVR-x,
+    every y within the oracle bar, the workspace (conversion counters included) back at rest, several launches."""
+    shapes = [(1024, 4096), (4096, 4096), (2048, 14336), (256, 384)]
+    probs_q, probs_s, refs = [], [], []
+    for i, (M, N) in enumerate(shapes):
+        pc, s16, b16, ri = synthetic.random_encoded(M, N, 4, 16, seed=500 + i)
+        w = sb.pack_canonical(pc, s16, b16, ri, 16)
+        x = synthetic.activation(N, seed=510 + i, outliers=8 if i == 1 else 0)[0]
+        xd = torch.from_numpy(x).to(DEV)
+        probs_q.append((w, sb.fp16q_activation(xd, l=l), torch.full((M,), float("nan"), device=DEV)))
+        probs_s.append((w, sb.encode_vector(xd, l=l), torch.full((M,), float("nan"), device=DEV)))
+        enc = oracle.Encoded(M, N, oracle.OracleConfig(K=4, n_ratio=16), pc, s16, b16, ri, None)
+        z, _, sc = oracle.encode_vector(x, 128, l)
+        refs.append(oracle.gemv_rows(enc, oracle.x_dec_sbvr(z, sc)))
+    ws = _CanaryWs(probs_q)
+    ys_s = sb.gemv_group(probs_s)
+    for it in range(3):
+        ys_q = sb.gemv_group(probs_q, ws=ws)
+        torch.cuda.synchronize()
+        assert ws.canary_ok()          # (the conversion scratch holds the converted x; counters re-armed: next launch)
+        for yq, ys in zip(ys_q, ys_s):
+            assert torch.equal(yq, ys)
+    for y, ref in zip(ys_q, refs):
+        _close(y.cpu().numpy(), ref)
