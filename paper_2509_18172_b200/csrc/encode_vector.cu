@@ -10,7 +10,13 @@
 
 namespace sbvr {
 
-__global__ void __launch_bounds__(256) encode_vector_kernel(const uint16_t* __restrict__ x, int total_groups, int l,
+#ifndef SBVR_ENCVEC_THREADS
+#define SBVR_ENCVEC_THREADS 32
+#endif
+// One warp per CTA by default: a CTA this small (~1K registers) fits beside a persistent GEMV CTA that leaves a few
+// registers of the SM free (sbvr_gemv_group), so the conversion never holds an SM that the GEMV of the next step
+// needs (256-thread CTAs took a whole SM from the grouped GEMV: its CTAs there started ~8 us late).
+__global__ void __launch_bounds__(SBVR_ENCVEC_THREADS) encode_vector_kernel(const uint16_t* __restrict__ x, int total_groups, int l,
                                                             uint32_t* __restrict__ planes,
                                                             float* __restrict__ scales) {
   // programmatic dependent launch: let the next kernel (the GEMV that reads our planes) be scheduled at once -- its
@@ -54,10 +60,10 @@ __global__ void __launch_bounds__(256) encode_vector_kernel(const uint16_t* __re
 sbvr_status launch_encode_vector(const uint16_t* x, int T, int N, int l, uint32_t* planes, float* scales,
                                  cudaStream_t st) {
   const int groups = T * (N / kG);
-  const int blocks = (groups * 32 + 255) / 256;
+  const int blocks = (groups * 32 + SBVR_ENCVEC_THREADS - 1) / SBVR_ENCVEC_THREADS;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(SBVR_ENCVEC_THREADS);
   cfg.stream = st;
   cudaLaunchAttribute attr_pdl[1];
   attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

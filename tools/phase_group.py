@@ -83,13 +83,13 @@ S = 5
 t = bufs[S].cpu().numpy().reshape(-1, 16)
 valid = t[:, 0] > 0
 base = t[valid, 0].min()
-n_cta = t.shape[0] // sb_warps if (sb_warps := 8) else 0
-done = np.where(valid, (t[:, 2] - base) / 1e3, np.nan).reshape(-1, 8)
-start = np.where(valid, (t[:, 0] - base) / 1e3, np.nan).reshape(-1, 8)
-first = np.where(valid, (t[:, 1] - base) / 1e3, np.nan).reshape(-1, 8)
-print("done by warp index:", [round(float(np.nanmean(done[:, w])), 2) for w in range(8)])
-print("loop time (done-first) by warp index:", [round(float(np.nanmean(done[:, w] - first[:, w])), 2) for w in range(8)])
-smid = t[:, 4].reshape(-1, 8)[:, 0]
+WPC = int(os.environ.get("WPC", "16"))           # warps per CTA of the build (SBVR_GROUP_WARPS)
+done = np.where(valid, (t[:, 2] - base) / 1e3, np.nan).reshape(-1, WPC)
+start = np.where(valid, (t[:, 0] - base) / 1e3, np.nan).reshape(-1, WPC)
+first = np.where(valid, (t[:, 1] - base) / 1e3, np.nan).reshape(-1, WPC)
+print("done by warp index:", [round(float(np.nanmean(done[:, w])), 2) for w in range(WPC)])
+print("loop time (done-first) by warp index:", [round(float(np.nanmean(done[:, w] - first[:, w])), 2) for w in range(WPC)])
+smid = t[:, 4].reshape(-1, WPC)[:, 0]
 cta_start = np.nanmin(start, axis=1)
 rank = np.zeros(len(smid), int)
 for sm in np.unique(smid):
