@@ -47,6 +47,13 @@ constexpr int kThreads = (kExpandWarps + kEpiWarps + kIssuerWarps) * 32;
 constexpr int kRing = 8;           // depth of the per-unit coefficient / token-scale ring (expansion -> epilogue)
 constexpr int kMaxPlanes = 4;
 constexpr int kMaxNT = 32;         // tokens per weight pass
+#ifndef ZT_AB_SLOTS
+#define ZT_AB_SLOTS 2
+#endif
+constexpr int kAS = ZT_AB_SLOTS;
+#ifndef ZT_MIN_UNITS
+#define ZT_MIN_UNITS 8
+#endif   // A (tensor memory) / B (shared memory) slots: units in flight between expansion and MMA
 constexpr unsigned int kSentinel = 0xFFFFFFFFu;
 
 struct ZtParams {
@@ -109,20 +116,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
   constexpr int kSlotBytes = (kUnitFull + 127) / 128 * 128;
   constexpr int kBBytes = 4 * NT * 32;           // B_q (q = 0..3): NT rows x 32 bytes each
   constexpr int TQ = NT / 2;                     // tokens per epilogue warp (2 per lane quarter)
-  constexpr int kDCol = 64 * K;                  // A_t[slot] at 64 t + 32 slot; D_t[buf] at kDCol + NT (t + K buf)
+  constexpr int kDCol = 32 * kAS * K;           // A_t[slot] at 32 (kAS t + slot); D_t[buf] at kDCol + NT (t + K buf)
   // D double-buffered when it fits (MMA(k) need not wait for the epilogue of unit k-1)
   constexpr int kDBuf = kDCol + 2 * K * NT <= 512 ? 2 : 1;
+  static_assert(kDCol + K * NT <= 512, "tensor memory: A slots + one D buffer exceed 512 columns");
   constexpr int TC = TQ < 8 ? TQ : 8;            // epilogue token chunk (K x TC registers per TMEM load round)
   constexpr uint32_t kIdesc = (2u << 4) | (1u << 10) | ((uint32_t)(NT >> 3) << 17) | (8u << 24);  // s32 += u8*s8, M=128
   constexpr int kE = kExpandWarps, kP = kEpiWarps;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
   uint8_t* sB = smem + kSlots * kSlotBytes;
-  float* s_c = reinterpret_cast<float*>(sB + 2 * kBBytes);      // [kRing][K][128] c_t = s r^t + b per row
+  float* s_c = reinterpret_cast<float*>(sB + kAS * kBBytes);      // [kRing][K][128] c_t = s r^t + b per row
   __shared__ float s_rpow[64 * kMaxPlanes];
   __shared__ __align__(8) uint64_t bar_full[kSlots];
-  __shared__ __align__(8) uint64_t bar_a[2];
-  __shared__ __align__(8) uint64_t bar_abfree[2];   // MMAs of a unit done (all planes): its A/B slots are free
+  __shared__ __align__(8) uint64_t bar_a[kAS];
+  __shared__ __align__(8) uint64_t bar_abfree[kAS];   // MMAs of a unit done (all planes): its A/B slots are free
   __shared__ __align__(8) uint64_t bar_dfull[kMaxPlanes][2];
   __shared__ __align__(8) uint64_t bar_dempty[kMaxPlanes][2];
   __shared__ unsigned int s_rel[kSlots];          // expansion warps done with a ring slot (the last refills it)
@@ -151,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
       mbar_init(&bar_full[s], 1);
       s_rel[s] = 0;
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kAS; ++s) {
       mbar_init(&bar_a[s], kE);
       mbar_init(&bar_abfree[s], K);
     }
@@ -181,20 +189,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
       PH_DECL
       const uint32_t bbase = smem_u32(sB);
       for (int k = 0; k < n; ++k) {
-        ZT_WAIT_CRIT(&bar_a[k & 1], (k >> 1) & 1);              // A_t / B of unit k are in place
+        ZT_WAIT_CRIT(&bar_a[k % kAS], (k / kAS) & 1);           // A_t / B of unit k are in place
         PH(0);
         const int db = k % kDBuf;
         if (k >= kDBuf)                                          // the epilogue has read D_t[db] of unit k - kDBuf
           mbar_wait_backoff(&bar_dempty[t][db], ((k / kDBuf) - 1) & 1);
         tc_fence_after();
         PH(1);
-        const uint32_t tA = tmem + 64 * t + 32 * (k & 1);
+        const uint32_t tA = tmem + 32 * (kAS * t + k % kAS);
         const uint32_t tD = tmem + kDCol + NT * (t + K * db);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (!(ZT_ABL & 4)) mma_i8_ts(tD, tA + 8 * q, smem_desc(bbase + (k & 1) * kBBytes + q * NT * 32, 128, 256), kIdesc, q);
+          if (!(ZT_ABL & 4)) mma_i8_ts(tD, tA + 8 * q, smem_desc(bbase + (k % kAS) * kBBytes + q * NT * 32, 128, 256), kIdesc, q);
         mma_commit(&bar_dfull[t][db]);
-        mma_commit(&bar_abfree[k & 1]);
+        mma_commit(&bar_abfree[k % kAS]);
         PH(2);
       }
       if (t == 0) PH_DUMP(16);
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
     int rb = V0 / NG, g = V0 - (V0 / NG) * NG;
     for (int k = 0; k < n; ++k) {
       const int rows = rows_of(rb);
-      if (k >= 2) ZT_WAIT_CRIT(&bar_abfree[k & 1], ((k - 2) >> 1) & 1);   // A_t[k&1], B[k&1] read by MMA(k-2)
+      if (k >= kAS) ZT_WAIT_CRIT(&bar_abfree[k % kAS], ((k - kAS) / kAS) & 1);   // slot read by MMA(k - kAS)
       PH(0);
       if (bwarp && !(ZT_ABL & 1)) {
         uint32_t Z[8];
@@ -252,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
           Z[j] ^= x << 4;
         }
         // register s, byte i = z(32 bq + 8 i + s) = k-order byte 4 s + i of B row bn (MMA q = bq)
-        uint8_t* row = sB + (k & 1) * kBBytes + bq * (NT * 32) + (bn >> 3) * 256 + (bn & 7) * 16;
+        uint8_t* row = sB + (k % kAS) * kBBytes + bq * (NT * 32) + (bn >> 3) * 256 + (bn & 7) * 16;
         *reinterpret_cast<uint4*>(row) = make_uint4(Z[0], Z[1], Z[2], Z[3]);
         *reinterpret_cast<uint4*>(row + 128) = make_uint4(Z[4], Z[5], Z[6], Z[7]);
         if (bq == 0) s_sx[k % kRing][bn] = sxn;
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
         for (int q = 0; q < 4; ++q)
 #pragma unroll
           for (int s = 0; s < 8; ++s) a[8 * q + s] = shr_fma(wq[q], s) & 0x01010101u;
-        tmem_st32(tmem + lane_base + 64 * sub + 32 * (k & 1), a);
+        tmem_st32(tmem + lane_base + 32 * (kAS * sub + k % kAS), a);
       }
       if (sub == K - 1) {                            // c_t = s r^t + b (Eq. 4) of this row, for the epilogue
         uint32_t sbw = 0, ri = 0;
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&bar_a[k & 1]);
+        mbar_arrive(&bar_a[k % kAS]);
         // the last expansion warp done with this slot refills it with unit k + kSlots
         if (atomicAdd(&s_rel[slot], 1u) == kE - 1) {
           s_rel[slot] = 0;
@@ -346,18 +354,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_zt_kernel(ZtParams p) {
           for (int cc = c0; cc <= c1; ++cc) {
             const int sl = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
             float* src = p.ws_part + ((size_t)cc * 2 + sl) * (NT * 128);
+            if (cc == cta) {
 #pragma unroll
-            for (int i = 0; i < TQ; ++i) {
-              float v = y[i];
-              if (cc != cta) {
-                uint32_t w;
-                long spins = 0;
-                while ((w = ld_relaxed_u32(src + (th * TQ + i) * 128 + r)) == kSentinel)
-                  if (++spins > (1L << 26)) __trap();   // stores already issued never landed
-                v = __uint_as_float(w);
-              }
-              sum[i] += v;
+              for (int i = 0; i < TQ; ++i) sum[i] += y[i];
+              continue;
             }
+            // all TQ words of the slot in one batch (one L2 round trip), reloaded while any is the sentinel
+            uint32_t w[TQ];
+            for (long spins = 0;; ++spins) {
+              bool miss = false;
+#pragma unroll
+              for (int i = 0; i < TQ; ++i) {
+                w[i] = ld_relaxed_u32(src + (th * TQ + i) * 128 + r);
+                miss |= w[i] == kSentinel;
+              }
+              if (!miss) break;
+              if (spins > (1L << 26)) __trap();          // stores already issued never landed
+            }
+#pragma unroll
+            for (int i = 0; i < TQ; ++i) sum[i] += __uint_as_float(w[i]);
           }
           for (int cc = c0; cc <= c1; ++cc) {
             const int sl = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
@@ -471,7 +486,10 @@ static Plan make_plan(const sbvr_weights* w) {
   pl.tail_rows = w->M % kRowBlock;
   pl.n_rb = pl.n_full + (pl.tail_rows ? 1 : 0);
   pl.Us = pl.n_rb * pl.NG;
-  pl.C = num_sms() < pl.Us ? num_sms() : pl.Us;
+  // at least ZT_MIN_UNITS units per CTA: a row block split over fewer CTAs has fewer partials to combine (the
+  // last-arriving CTA reads one slot per contributor), which dominates small matrices at large T
+  const int by_units = (pl.Us + ZT_MIN_UNITS - 1) / ZT_MIN_UNITS;
+  pl.C = num_sms() < by_units ? num_sms() : (by_units < 1 ? 1 : by_units);
   return pl;
 }
 
@@ -480,7 +498,7 @@ static size_t cnt_bytes(const Plan& pl) { return ((size_t)(pl.n_rb + 1) * 4 + 25
 
 template <int K, int NT, bool DEBUG>
 static cudaError_t launch_one(const ZtParams& p, int C, cudaStream_t st) {
-  const int smem = kSlots * ((128 * (16 * K + 5) + 127) / 128 * 128) + 2 * 4 * NT * 32 + kRing * K * 128 * 4;
+  const int smem = kSlots * ((128 * (16 * K + 5) + 127) / 128 * 128) + kAS * 4 * NT * 32 + kRing * K * 128 * 4;
   static bool attr[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
