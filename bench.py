@@ -606,6 +606,37 @@ def _record(sb, device, config, name, M, N, K, T, act_kind, algo, P=1, M_full=No
     return rec
 
 
+def _group_record(sb, device, config, mats, P=1, iters=30, seed=0):
+    """A SURVEY §8d.8-style record for one grouped launch (sbvr_gemv_group) over the matrices `mats` [(name, M, N)]
+    (this rank's row shards at P ranks): us per launch median/p10/p90 over graph replays on a ring of distinct
+    weight sets (> L2), algorithmic GB/s and fractions of 8 TB/s and of the measured copy peak."""
+    sets, byts = [], 0
+    base = []
+    for j, (name, M, N) in enumerate(mats):
+        pc, s16, b16, ri = synthetic.random_encoded(M, N, K_BITS, N_RATIO, seed=seed + 31 * j + M + N)
+        base.append(sb.pack_canonical(pc, s16, b16, ri, N_RATIO, device=device))
+        byts += sb.algorithmic_bytes(M, N, K_BITS, act="sbvr", l=L_BITS)
+    ring = _ring_count(sum(w.nbytes for w in base))
+    xs = [sb.encode_vector(torch.from_numpy(synthetic.activation(N, seed=60 + j)).to(device))
+          for j, (_, M, N) in enumerate(mats)]
+    ys = [torch.empty(M, dtype=torch.float32, device=device) for (_, M, N) in mats]
+    for r in range(ring):
+        ws_ = base if r == 0 else [sb.SbvrWeights(w.M, w.N, K_BITS, N_RATIO, w.data.clone(), w.ratio_pow.clone())
+                                   for w in base]
+        probs = [(w, x, y) for w, x, y in zip(ws_, xs, ys)]
+        sets.append((probs, sb.group_workspace(probs)))
+    stream = torch.cuda.Stream(device)
+    med, p10, p90 = _graph_stats(stream, lambda i: sb.gemv_group(sets[i % ring][0], ws=sets[i % ring][1]), iters)
+    del sets
+    torch.cuda.empty_cache()
+    peak, _ = measured_peak()
+    gbps = byts / (med * 1e-6) / 1e9
+    return {"config": config, "shape": "+".join(f"{n} {M}x{N}" for n, M, N in mats), "K": K_BITS, "l": L_BITS,
+            "path": "SBVR-x/group", "T": 1, "P": P, "bytes_alg": int(byts), "us_median": round(med, 3),
+            "us_p10": round(p10, 3), "us_p90": round(p90, 3), "GBps": round(gbps, 1), "pct_8TBps": round(gbps / 80.0, 2),
+            "pct_measured_peak": round(100 * gbps / peak, 2), "ring": ring}
+
+
 def records(device):
     """one record per (config, shape, K, path, T, P) -- C2 Llama-3-8B decode set, C3 Llama-3-70B
     MLP row shards, C4 Qwen2.5-7B K sweep on both activation paths, C5 batched T = 1..64 -- plus f3."""
@@ -617,6 +648,13 @@ def records(device):
         for P in (1, 2, 4, 8):
             out.append(_record(sb, device, "C3 llama3_70b_mlp_row_shard", name, M // P, N, K_BITS, 1, "sbvr",
                                sb.ALGO_AUTO, P=P, M_full=M, iters=40))
+    # C3 per-rank MLP GEMVs as one grouped launch (fused gate_up + down row shards), P = 1/2/4/8 on one GPU
+    for P in (1, 2, 4, 8):
+        out.append(_group_record(sb, device, "C3 llama3_70b_mlp_row_shard_grouped",
+                                 [("gate_up_proj", 57344 // P, 8192), ("down_proj", 8192 // P, 28672)], P=P,
+                                 iters=20 if P <= 2 else 40))
+    # C2 layer set as one grouped launch (the bench step's GEMV part, one launch per graph node)
+    out.append(_group_record(sb, device, "C2 llama3_8b_grouped", [(n, M, N) for n, M, N, _, _ in FUSED], iters=40))
     for name, M, N in (("q_proj", 3584, 3584), ("k_proj", 512, 3584), ("gate_proj", 18944, 3584), ("down_proj", 3584, 18944)):
         for K in (2, 3, 4):
             for kind in ("sbvr", "fp16"):
