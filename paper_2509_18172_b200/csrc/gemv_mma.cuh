@@ -62,7 +62,10 @@ inline int cur_device() {
 #define SBVR_MMA_WARPS 8
 #endif
 constexpr int kImmaWarps = SBVR_MMA_WARPS;   // warps per CTA (two CTAs per SM fill the register file)
-constexpr int kMinUnitsPerCta = 2;   // small problems: spread over SMs, at least this many units per CTA
+#ifndef SBVR_MMA_MIN_UNITS
+#define SBVR_MMA_MIN_UNITS 4
+#endif
+constexpr int kMinUnitsPerCta = SBVR_MMA_MIN_UNITS;   // small problems: spread over SMs, at least this many units per CTA
 #ifndef SBVR_MMA_CTAS_PER_SM
 #define SBVR_MMA_CTAS_PER_SM 2     // resident CTAs per SM: two 8-warp CTAs (profiles/r02_cta_shape_ab.txt)
 #endif
