@@ -849,6 +849,19 @@ def encode_throughput(device):
            "shape": "4096x4096", "seconds": s, "groups_per_s": groups / s, "params_per_s": groups * G / s,
            "search_space": "16x64x16 (R x S x B), strict fp64",
            "full_llama3_8b_extrapolated_s": 54525952 / (groups / s)}
+    # fast mode (strict = 0): fp32 scan + fp64 re-evaluation of the near-best entries
+    a.record()
+    w_fast, m_fast = sb.encode_weights(W, K=K_BITS, return_mse=True, strict=False)
+    b.record()
+    torch.cuda.synchronize()
+    sf = a.elapsed_time(b) / 1e3
+    w_strict = sb.encode_weights(W, K=K_BITS)
+    torch.cuda.synchronize()
+    out["fast"] = {"seconds": round(sf, 3), "groups_per_s": round(groups / sf), "speedup_vs_strict": round(s / sf, 2),
+                   "identical_to_strict": bool(torch.equal(w_fast.data, w_strict.data)),
+                   "mean_mse": m_fast.mean().item(), "mean_mse_strict": m_full_all.mean().item(),
+                   "full_llama3_8b_extrapolated_s": round(54525952 / (groups / sf), 1)}
+    del w_fast, w_strict
     # f2: the encode-time coefficient cache (per-row MRU cache of 8, moving-average admission)
     _, m_full = sb.encode_weights(W[:512].contiguous(), K=K_BITS, return_mse=True)
     a.record()

@@ -112,7 +112,11 @@ typedef struct {
   int32_t n_scale;       /* |S|, 1..4096 */
   int32_t n_bias;        /* |B|, 1..4096 */
   double s_min_factor;   /* s_min = s_min_factor * q95(D); 2.0 = paper Eq. 10 */
-  int32_t strict;        /* 1 = fp64 search bit-identical to the oracle (only mode in this build) */
+  int32_t strict;        /* 1 = fp64 search bit-identical to the oracle; 0 = fast (sbvr_encode_weights only): every
+                            entry's MSE in fp32, then the strict fp64 MSE of the entries within a margin of the fp32
+                            best and their strict arg-min in entry order (SURVEY §8c.5 contract: the choice's fp64
+                            MSE <= (1 + 1e-6) x the strict best; planes = the nearest assignment for the chosen
+                            coefficients, computed in fp64 as in strict mode) */
 } sbvr_encode_config;
 
 /* Per-group coefficient metadata of a weight buffer. */

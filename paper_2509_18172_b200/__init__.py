@@ -241,12 +241,14 @@ _DT = {torch.float32: F32, torch.float16: F16, torch.bfloat16: BF16}
 
 
 def encode_weights(W: torch.Tensor, K: int = 4, n_ratio: int = 16, n_scale: int = 64, n_bias: int = 16,
-                   s_min_factor: float = 2.0, return_mse: bool = False, out: Optional[SbvrWeights] = None):
-    """sbvr_encode_weights: W is a CUDA [M, N] fp32/fp16/bf16 tensor."""
+                   s_min_factor: float = 2.0, return_mse: bool = False, out: Optional[SbvrWeights] = None,
+                   strict: bool = True):
+    """sbvr_encode_weights: W is a CUDA [M, N] fp32/fp16/bf16 tensor.  strict=False: the fast search
+    (fp32 scan, fp64 re-evaluation of the near-best entries; include/sbvr.h)."""
     assert W.is_cuda and W.dim() == 2 and W.is_contiguous()
     M, N = W.shape
     w = out if out is not None else weights_empty(M, N, K, n_ratio, W.device)
-    cfg = _EncCfg(K, G, n_ratio, n_scale, n_bias, float(s_min_factor), 1)
+    cfg = _EncCfg(K, G, n_ratio, n_scale, n_bias, float(s_min_factor), 1 if strict else 0)
     mse = torch.empty((M, N // G), dtype=torch.float64, device=W.device) if return_mse else None
     d = w.desc()
     _check(lib().sbvr_encode_weights(ctypes.byref(cfg), _ptr(W), _DT[W.dtype], M, N, ctypes.byref(d), _ptr(mse),
@@ -256,13 +258,13 @@ def encode_weights(W: torch.Tensor, K: int = 4, n_ratio: int = 16, n_scale: int 
 
 def encode_weights_cached(W: torch.Tensor, K: int = 4, cache_size: int = 8, ema_alpha: float = 0.1, n_ratio: int = 16,
                           n_scale: int = 64, n_bias: int = 16, s_min_factor: float = 2.0,
-                          out: Optional[SbvrWeights] = None):
-    """sbvr_encode_weights_cached: the encode-time coefficient cache.  Returns (weights, group
-    MSE [M, N/G] fp64, hit [M, N/G] uint8)."""
+                          out: Optional[SbvrWeights] = None, strict: bool = True):
+    """sbvr_encode_weights_cached: the encode-time coefficient cache (strict only).  Returns (weights,
+    group MSE [M, N/G] fp64, hit [M, N/G] uint8)."""
     assert W.is_cuda and W.dim() == 2 and W.is_contiguous()
     M, N = W.shape
     w = out if out is not None else weights_empty(M, N, K, n_ratio, W.device)
-    cfg = _EncCfg(K, G, n_ratio, n_scale, n_bias, float(s_min_factor), 1)
+    cfg = _EncCfg(K, G, n_ratio, n_scale, n_bias, float(s_min_factor), 1 if strict else 0)
     mse = torch.empty((M, N // G), dtype=torch.float64, device=W.device)
     hit = torch.empty((M, N // G), dtype=torch.uint8, device=W.device)
     d = w.desc()

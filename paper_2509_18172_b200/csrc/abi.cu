@@ -138,7 +138,6 @@ static sbvr_status check_encode(const sbvr_encode_config* cfg, const void* W, in
     return set_error(SBVR_ERR_INVALID_ARG, "n_ratio=%d must be even in 2..64", cfg->n_ratio);
   if (cfg->n_scale < 1 || cfg->n_scale > 4096 || cfg->n_bias < 1 || cfg->n_bias > 4096)
     return set_error(SBVR_ERR_INVALID_ARG, "n_scale/n_bias outside 1..4096");
-  if (!cfg->strict) return set_error(SBVR_ERR_UNSUPPORTED, "only strict (fp64, oracle-exact) encoding is built");
   if (out->M != M || out->N != N || out->K != cfg->K || out->group_size != cfg->group_size ||
       out->n_ratio != cfg->n_ratio)
     return set_error(SBVR_ERR_SHAPE, "output descriptor does not match M/N/K/group_size/n_ratio");
@@ -150,7 +149,7 @@ sbvr_status sbvr_encode_weights(const sbvr_encode_config* cfg, const void* W, in
   sbvr_status s = check_encode(cfg, W, dtype, M, N, out);
   if (s != SBVR_OK) return s;
   if (out->meta_kind != SBVR_META_GROUP) return set_error(SBVR_ERR_INVALID_ARG, "out must be SBVR_META_GROUP");
-  return launch_encode_weights(cfg, W, dtype, M, N, out, group_mse, -1, 0.0, nullptr, (cudaStream_t)stream);
+  return launch_encode_weights(cfg, W, dtype, M, N, out, group_mse, -1, 0.0, nullptr, (cudaStream_t)stream);   // strict or fast
 }
 
 sbvr_status sbvr_encode_weights_indexed(const sbvr_encode_config* cfg, int32_t n_table, const void* W, int32_t dtype,
@@ -158,6 +157,7 @@ sbvr_status sbvr_encode_weights_indexed(const sbvr_encode_config* cfg, int32_t n
                                         void* workspace, size_t ws_bytes, void* stream) {
   sbvr_status s = check_encode(cfg, W, dtype, M, N, out);
   if (s != SBVR_OK) return s;
+  if (!cfg->strict) return set_error(SBVR_ERR_UNSUPPORTED, "the indexed encoder runs strict (fp64) only");
   if (out->meta_kind != SBVR_META_INDEXED) return set_error(SBVR_ERR_INVALID_ARG, "out must be SBVR_META_INDEXED");
   if (n_table < 1 || n_table > kMaxTable) return set_error(SBVR_ERR_INVALID_ARG, "n_table=%d outside 1..256", n_table);
   if (!workspace || ws_bytes < (size_t)8 * n_table)
@@ -172,6 +172,7 @@ sbvr_status sbvr_encode_weights_cached(const sbvr_encode_config* cfg, int32_t ca
   sbvr_status s = check_encode(cfg, W, dtype, M, N, out);
   if (s != SBVR_OK) return s;
   if (out->meta_kind != SBVR_META_GROUP) return set_error(SBVR_ERR_INVALID_ARG, "out must be SBVR_META_GROUP");
+  if (!cfg->strict) return set_error(SBVR_ERR_UNSUPPORTED, "the cached encoder runs strict (fp64) only");
   if (cache_size < 0 || cache_size > 64) return set_error(SBVR_ERR_INVALID_ARG, "cache_size=%d outside 0..64", cache_size);
   if (!(ema_alpha > 0.0 && ema_alpha <= 1.0)) return set_error(SBVR_ERR_INVALID_ARG, "ema_alpha outside (0, 1]");
   return launch_encode_weights(cfg, W, dtype, M, N, out, group_mse, cache_size, ema_alpha, group_hit,

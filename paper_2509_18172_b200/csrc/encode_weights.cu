@@ -57,6 +57,8 @@ struct EncParams {
   uint8_t* data;
   double* group_mse;
   uint8_t* group_hit;     // cached encoder: 1 = the group took a cached coefficient set
+  int fast;               // 1: fp32 search of every entry, fp64 (strict) re-evaluation of the near-best ones
+  int m32_cap;            // fast mode: entries whose fp32 MSE fits in dynamic shared memory
   int cache_size;         // cached encoder: MRU capacity (0..64)
   double cache_alpha;     // cached encoder: moving-average weight
 };
@@ -193,6 +195,100 @@ __device__ void grp_search(const EncParams& p, const GroupSmem& sm, double* red_
   __syncthreads();
 }
 
+// Fast mode (sbvr_encode_config.strict = 0): the same MSE in fp32 (same formula, fp32 rounding).
+template <int K>
+__device__ __forceinline__ float entry_mse32(const double* X, float r, float s, float b) {
+  constexpr int NPTS = 1 << K;
+  float c[K];
+  float pw = 1.f;
+#pragma unroll
+  for (int t = 0; t < K; ++t) {
+    c[t] = fmaf(s, pw, b);
+    pw *= r;
+  }
+  float v[NPTS];
+#pragma unroll
+  for (int m = 0; m < NPTS; ++m) {
+    float acc = 0.f;
+#pragma unroll
+    for (int t = 0; t < K; ++t)
+      if ((m >> t) & 1) acc += c[t];
+    v[m] = acc;
+  }
+  float sse = 0.f;
+#pragma unroll 4
+  for (int el = 0; el < kG; ++el) {
+    const float x = (float)X[el];
+    float d = fabsf(x - v[0]);
+#pragma unroll
+    for (int m = 1; m < NPTS; ++m) d = fminf(d, fabsf(x - v[m]));
+    sse = fmaf(d, d, sse);
+  }
+  return sse * (1.0f / kG);
+}
+
+// Fast-mode Algorithm 1: pass 1 evaluates every entry in fp32 (kept in shared memory when the space fits);
+// pass 2 re-evaluates, with the strict fp64 entry_mse, every entry whose fp32 MSE is within a margin of the fp32
+// best (the margin covers the fp32 error of a 128-term SSE many times over), and takes the strict arg-min of those
+// in entry order.  Whenever the strict winner is in that set -- the margin makes that the rule -- the result is
+// bit-identical to strict mode; the §8c.5 contract (strict MSE of the choice <= (1 + 1e-6) x the strict best) holds
+// regardless of ties at the margin.
+template <int K>
+__device__ void grp_search_fast(const EncParams& p, const GroupSmem& sm, float* m32, int m32_cap, double* red_mse,
+                                int* red_e, int* win_e, double* win_mse) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int E = p.n_ratio * p.n_scale * p.n_bias, SB = p.n_scale * p.n_bias;
+  const bool keep = E <= m32_cap;
+  float best32 = FLT_MAX, x2max = 0.f;
+  for (int el = lane; el < kG; el += 32) x2max = fmaxf(x2max, (float)(sm.X[el] * sm.X[el]));
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int i = e / SB, rem = e - i * SB, j = rem / p.n_bias, k = rem - j * p.n_bias;
+    const float m = entry_mse32<K>(sm.X, (float)sm.R[i], (float)sm.S[j], (float)sm.B[k]);
+    if (keep) m32[e] = m;
+    best32 = fminf(best32, m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    best32 = fminf(best32, __shfl_xor_sync(0xffffffffu, best32, o));
+    x2max = fmaxf(x2max, __shfl_xor_sync(0xffffffffu, x2max, o));
+  }
+  float* red32 = reinterpret_cast<float*>(red_mse);
+  __syncthreads();
+  if (lane == 0) red32[warp] = best32;
+  __syncthreads();
+  float b32 = red32[0];
+  for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b32 = fminf(b32, red32[w]);
+  const float thr = b32 * (1.f + 1.f / 1024.f) + x2max * (1.f / (1 << 20));
+  __syncthreads();
+  double best = DBL_MAX;
+  int best_e = 0x7fffffff;
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int i = e / SB, rem = e - i * SB, j = rem / p.n_bias, k = rem - j * p.n_bias;
+    const float m = keep ? m32[e] : entry_mse32<K>(sm.X, (float)sm.R[i], (float)sm.S[j], (float)sm.B[k]);
+    if (m <= thr) {
+      const double mse = entry_mse<K>(sm.X, sm.R[i], sm.S[j], sm.B[k]);
+      if (mse < best) { best = mse; best_e = e; }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double om = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oe = __shfl_xor_sync(0xffffffffu, best_e, o);
+    if (om < best || (om == best && oe < best_e)) { best = om; best_e = oe; }
+  }
+  if (lane == 0) { red_mse[warp] = best; red_e[warp] = best_e; }
+  __syncthreads();
+  if (tid == 0) {
+    double bm = red_mse[0];
+    int be = red_e[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (red_mse[w] < bm || (red_mse[w] == bm && red_e[w] < be)) { bm = red_mse[w]; be = red_e[w]; }
+    *win_e = be;
+    *win_mse = bm;
+  }
+  __syncthreads();
+}
+
 // P:231 bit assignment for coefficients (r, s, b) and the stores of planes / meta / mse.
 template <int K>
 __device__ void grp_assign_store(const EncParams& p, const GroupSmem& sm, int row, int g, double r, double s, double b,
@@ -246,6 +342,9 @@ __global__ void __launch_bounds__(256) encode_weights_kernel(EncParams p) {
   sm.R = sm.Xs + kG;
   sm.S = sm.R + 64;
   sm.B = sm.S + p.n_scale;
+  // fast mode: the fp32 MSE of every entry, after the candidate sets (m32_cap entries; 0 in strict mode)
+  float* m32 = reinterpret_cast<float*>(sm.B + p.n_bias);
+  const int m32_cap = p.fast ? p.m32_cap : 0;
   __shared__ double s_scal[4];       // s_min, s_gran, b_min, b_gran
   __shared__ double red_mse[8];
   __shared__ int red_e[8];
@@ -262,7 +361,10 @@ __global__ void __launch_bounds__(256) encode_weights_kernel(EncParams p) {
     const int row = (int)(q / Lo.NG), g = (int)(q % Lo.NG);
     grp_load(p, sm, row, g);
     grp_candidates<K>(p, sm, s_scal);
-    grp_search<K>(p, sm, red_mse, red_e, &win_e, &win_mse);
+    if (p.fast)
+      grp_search_fast<K>(p, sm, m32, m32_cap, red_mse, red_e, &win_e, &win_mse);
+    else
+      grp_search<K>(p, sm, red_mse, red_e, &win_e, &win_mse);
     const int we = win_e;
     const int wi = we / SB, wrem = we - wi * SB, wj = wrem / p.n_bias, wk = wrem - wj * p.n_bias;
     grp_assign_store<K>(p, sm, row, g, sm.R[wi], sm.S[wj], sm.B[wk], wi, win_mse, 0);
@@ -515,8 +617,11 @@ sbvr_status launch_ratio_table(float* ratio_pow, int n_ratio, int K, cudaStream_
 }
 
 template <int K>
-static sbvr_status launch_k(const EncParams& p, bool cached, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (2 * kG + 64 + p.n_scale + p.n_bias);
+static sbvr_status launch_k(const EncParams& p_in, bool cached, cudaStream_t st) {
+  EncParams p = p_in;
+  const long E = (long)p.n_ratio * p.n_scale * p.n_bias;
+  p.m32_cap = (p.fast && !cached) ? (int)(E <= 32768 ? E : 0) : 0;   // <= 128 KB of fp32 MSEs, else recomputed
+  const size_t smem = sizeof(double) * (2 * kG + 64 + p.n_scale + p.n_bias) + sizeof(float) * p.m32_cap;
   if (smem > 48 * 1024 - 2048) {
     cudaError_t e = cudaFuncSetAttribute(encode_weights_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -548,6 +653,8 @@ sbvr_status launch_encode_weights(const sbvr_encode_config* cfg, const void* W, 
   p.s_min_factor = cfg->s_min_factor;
   p.data = out->data;
   p.group_mse = group_mse;
+  p.fast = cfg->strict ? 0 : 1;
+  p.m32_cap = 0;
   sbvr_status s;
   switch (cfg->K) {
     case 1: s = launch_k<1>(p, cached, st); break;
