@@ -200,6 +200,12 @@ sbvr_status sbvr_gemv_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* 
     const size_t d = zt_workspace_bytes(w, T);
     if (d > *bytes) *bytes = d;
   }
+  if (w->M % kRowBlock == 0) {           // the grouped kernel serves large batch-1 GEMVs (sbvr_gemv_ex AUTO)
+    sbvr_gemv_problem pr = {};
+    pr.w = *w;
+    const size_t e = group_workspace_bytes(&pr, 1);
+    if (e > *bytes) *bytes = e;
+  }
   return SBVR_OK;
 }
 
@@ -249,13 +255,24 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
       return set_error(SBVR_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, need);
     return launch_gemv_mma(w, X, T, Y, workspace, ws_bytes, nullptr, st);
   }
+  // diagnostics only (A/B timing in tools/): SBVR_FORCE_ALGO=<sbvr_algo> overrides AUTO for SBVR-x
+  static const int forced = getenv("SBVR_FORCE_ALGO") ? atoi(getenv("SBVR_FORCE_ALGO")) : 0;
   if (algo == SBVR_ALGO_AUTO) {
-    // diagnostics only (A/B timing in tools/): SBVR_FORCE_ALGO=<sbvr_algo> overrides AUTO for SBVR-x
-    static const int forced = getenv("SBVR_FORCE_ALGO") ? atoi(getenv("SBVR_FORCE_ALGO")) : 0;
     if (forced > 0 && forced <= SBVR_ALGO_ZT && !(forced == SBVR_ALGO_PIPE && T != 1)) algo = forced;
   }
   if (algo == SBVR_ALGO_POPC) return launch_gemv_popc(w, X, T, Y, nullptr, st);
   if (algo == SBVR_ALGO_AUTO) {
+    // batch 1 on a large matrix (>= 2^26 weights, e.g. a 70B MLP projection): the grouped kernel with one problem
+    // (whole 128-row unit records, one copy per warp pair; measured 4-7 % faster there, slower on small shapes)
+    if (T == 1 && !forced && w->meta_kind == SBVR_META_GROUP && w->K >= 2 && w->K <= 4 && w->M % kRowBlock == 0 &&
+        (long)w->M * w->N >= (1L << 26)) {
+      sbvr_gemv_problem pr;
+      pr.w = *w;
+      pr.x = *X;
+      pr.y = Y;
+      const size_t need = group_workspace_bytes(&pr, 1);
+      if (workspace && ws_bytes >= need) return launch_gemv_group(&pr, 1, workspace, ws_bytes, st);
+    }
     // batches: the tcgen05 z-column kernel (one weight pass per 32 tokens) from zt_min tokens on; batch 1-2:
     // the mma.sync bit-plane kernel.  SBVR_ZT_MIN_T overrides the switch point (A/B timing).
     static const int zt_min = getenv("SBVR_ZT_MIN_T") ? atoi(getenv("SBVR_ZT_MIN_T")) : 12;

@@ -33,7 +33,7 @@ def test_fused_conversion_bit_identical(M, N, K, l):
         x[0, 128:256] = 0                                    # an all-zero group
         x[0, 300] = 127.0
     xd = torch.from_numpy(x[0]).to(DEV)
-    ref = sb.gemv(w, sb.encode_vector(xd, l=l))
+    ref = sb.gemv_ex(w, sb.encode_vector(xd, l=l), algo=sb.ALGO_MMA)[0]   # same kernel (AUTO may pick the grouped one)
     y = sb.gemv(w, sb.fp16q_activation(xd, l=l))
     torch.cuda.synchronize()
     assert torch.equal(y, ref)
@@ -55,7 +55,7 @@ def test_fused_conversion_indexed_and_peers():
     w = sb.pack_canonical(pc, s16, b16, ri, 16)
     full = torch.full((1, 2 * M), float("nan"), device=DEV)
     sb.gemv_to_peers(w, sb.fp16q_activation(xd), [full.data_ptr()], M, 2 * M)
-    ref = sb.gemv(w, sb.encode_vector(xd))
+    ref = sb.gemv_ex(w, sb.encode_vector(xd), algo=sb.ALGO_MMA)[0]
     torch.cuda.synchronize()
     assert torch.equal(a, b)
     assert torch.equal(full[0, M:], ref) and torch.isnan(full[0, :M]).all()
