@@ -764,6 +764,48 @@ def layer_chain(sb, device, reps=20):
                       "x32_layers_ms": round(32 * us / 1e3, 3)}
         del layers, acts
         torch.cuda.empty_cache()
+    # unfused weights, launched by dependency level with the grouped kernel: (q, k, v) -> o -> (gate, up) -> down,
+    # each level's inputs converted by one sbvr_encode_vector (q/k/v share x, gate/up share x): 4 + 4 launches,
+    # the fused form's launch count without stacking the weights
+    levels = [[0, 1, 2], [3], [4, 5], [6]]
+    ring = 3
+    layers = []
+    for r in range(ring):
+        ws_ = []
+        for i, (n, M, N) in enumerate(unf):
+            pc, s16, b16, ri = synthetic.random_encoded(M, N, K_BITS, N_RATIO, seed=900 + 13 * r + i)
+            ws_.append((sb.pack_canonical(pc, s16, b16, ri, N_RATIO, device=device), torch.empty(M, device=device)))
+        layers.append(ws_)
+    xs = [torch.from_numpy(synthetic.activation(unf[lv[0]][2], seed=lv[0])).to(device) for lv in levels]
+    acts = [sb.encode_vector(x) for x in xs]
+    probs = [[[(layers[r][i][0], acts[li], layers[r][i][1]) for i in lv] for li, lv in enumerate(levels)]
+             for r in range(ring)]
+    gws = [[sb.group_workspace(pl) for pl in probs[r]] for r in range(ring)]
+    stream = torch.cuda.Stream(device)
+    with torch.cuda.stream(stream):
+        def one_g(r):
+            for li in range(len(levels)):
+                sb.encode_vector(xs[li], out=acts[li])
+                sb.gemv_group(probs[r][li], ws=gws[r][li])
+        for r in range(ring):
+            one_g(r)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(reps):
+                one_g(i % ring)
+        g.replay()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+    us = a.elapsed_time(b) * 1e3 / reps
+    byts = sum(sb.algorithmic_bytes(M, N, K_BITS, act="sbvr", l=L_BITS, T=1) for (_, M, N) in unf)
+    out["unfused_7_grouped_by_level"] = {"us_per_layer": round(us, 2), "launches_per_layer": 8,
+                                         "GBps": round(byts / (us * 1e-6) / 1e9, 1), "x32_layers_ms": round(32 * us / 1e3, 3)}
+    del layers, acts, probs, gws
+    torch.cuda.empty_cache()
     return out
 
 
