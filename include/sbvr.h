@@ -251,7 +251,10 @@ sbvr_status sbvr_gemv_to_peers(const sbvr_weights* w, const sbvr_act* X, int32_t
  *          value) and y (device fp32 [M]).  No problem may write a buffer another problem reads (y's must not
  *          overlap x, scales or weights); y's must not overlap each other.
  *   Supported: SBVR_ACT_SBVR activations (T = 1, the same l for all), SBVR_META_GROUP weights, K in 2..4 and equal
- *   for all problems, M % 128 == 0 (SBVR_ERR_UNSUPPORTED / SBVR_ERR_SHAPE otherwise).
+ *   for all problems, M % 128 == 0 (SBVR_ERR_UNSUPPORTED / SBVR_ERR_SHAPE otherwise).  SBVR_ACT_FP16_Q activations
+ *   (all problems): the kernel converts every x itself (Eq. 12, bit-identical to sbvr_encode_vector) with a
+ *   grid-wide arrival count between conversion and use -- the grid is sized to the co-resident CTA count the
+ *   driver reports, so it must not share the GPU with another kernel that waits on this one.
  *   workspace: >= sbvr_gemv_group_workspace_bytes bytes, initialised once with sbvr_workspace_init and left at
  *   rest by every call; not shared with a concurrently running GEMV.
  * Arithmetic and per-band reduction order are those of sbvr_gemv's MMA kernel; y is deterministic. */
