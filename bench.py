@@ -268,8 +268,12 @@ def run_sbvr(args, world, rank, local_rank, pg):
                 off += r1 - r0
             ys.append(views)
         yfull = [torch.zeros(M, dtype=torch.float32, device=device) for (_, M, N, _, _) in FUSED]
-        symm = None
-        if args.allgather == "symm":                   # (at N = 1 too: exercises the same code path)
+        symm = symm_group = None
+        if args.allgather == "symm" and args.step == "group":   # grouped launch with the all-gather in its epilogue
+            symm_group = [sdist.SymmGroupRowShardedGemv([w for (_, M, N, r0, r1, w, ws, xin) in mats],
+                                                        [M for (_, M, N, r0, r1, w, ws, xin) in mats], pg)
+                          for mats in layers]
+        elif args.allgather == "symm":                 # (at N = 1 too: exercises the same code path)
             symm = [[sdist.SymmRowShardedGemv(w, M, 1, pg, ws) for (_, M, N, r0, r1, w, ws, xin) in mats]
                     for mats in layers]
         y_host = [torch.zeros(M, dtype=torch.float32).pin_memory() for (_, M, N, _, _) in FUSED]
@@ -299,10 +303,13 @@ def run_sbvr(args, world, rank, local_rank, pg):
         if group_probs is not None:
             if events is not None:
                 cr.record_external(events[0][0], stream)
-            sb.gemv_group(group_probs[r], ws=group_ws[r])
+            if symm_group is not None:
+                symm_group[r]([p[1] for p in group_probs[r]])
+            else:
+                sb.gemv_group(group_probs[r], ws=group_ws[r])
             if events is not None:
                 cr.record_external(events[0][1], stream)
-            if world > 1:
+            if world > 1 and symm_group is None:
                 for j in range(len(layers[r])):
                     sdist.all_gather_rows_into(yfull[j], ys[r][j], group=pg)
         for j, (name, M, N, r0, r1, w, ws, xin) in enumerate(layers[r] if group_probs is None else []):
@@ -323,7 +330,8 @@ def run_sbvr(args, world, rank, local_rank, pg):
             cr.record_external(span[1], stream)
         if e2e:
             for j in range(len(layers[r])):
-                src = symm[r][j].y_full[0] if symm is not None else (yfull[j] if world > 1 else ys[r][j])
+                src = (symm[r][j].y_full[0] if symm is not None else symm_group[r].y_full[j] if symm_group is not None
+                       else (yfull[j] if world > 1 else ys[r][j]))
                 y_host[j].copy_(src, non_blocking=True)
 
     # --- capture graphs: one plain step graph per ring layer; span-instrumented copies (one event
@@ -372,7 +380,7 @@ def run_sbvr(args, world, rank, local_rank, pg):
         # device -> host on a side stream, the next step's input while this step computes, this step's y while the
         # next one computes (per-step input buffers; one contiguous y per step).  Variants whose GEMVs read the fp16
         # input buffer directly (in-kernel conversion) or gather y across ranks keep the serial form below.
-        e2e_pipelined = (world == 1 and symm is None and not args.fused_conversion and
+        e2e_pipelined = (world == 1 and symm is None and symm_group is None and not args.fused_conversion and
                          not (group_probs is not None and args.xconv == "kernel"))
         e2e_multi = torch.cuda.CUDAGraph()
         if e2e_pipelined:
@@ -960,7 +968,7 @@ def main():
     ap.add_argument("--no-encode", action="store_true")
     ap.add_argument("--no-sweeps", action="store_true")
     args = ap.parse_args()
-    if args.allgather == "symm" or args.fused_conversion or args.chain:
+    if args.fused_conversion or args.chain:
         args.step = "chain"                        # those variants exist on the per-GEMV launches only
 
     world = env_int("WORLD_SIZE", 1)

@@ -267,6 +267,17 @@ typedef struct {
 sbvr_status sbvr_gemv_group_workspace_bytes(const sbvr_gemv_problem* probs, int32_t n, size_t* bytes);
 sbvr_status sbvr_gemv_group(const sbvr_gemv_problem* probs, int32_t n, void* workspace, size_t ws_bytes, void* stream);
 
+/* sbvr_gemv_group_to_peers -- sbvr_gemv_group over this rank's row shards with the all-gather fused into the
+ * epilogue (north star "row-sharded multi-GPU path ... joins y"): every y value of problem i is stored
+ * into each of the n_peers (1..8) buffers peer_y[i * n_peers + j] -- device pointers, typically every rank's
+ * symmetric-memory full y of problem i, [M_full[i]] fp32 each -- at row y_row_offset[i] + row; probs[i].y is ignored.
+ * peer_y, y_row_offset and M_full are HOST arrays.  The caller orders the stores before any read of a full y on
+ * another rank (signal-pad barrier, dist.py).  Same arithmetic, partition and determinism as sbvr_gemv_group; the
+ * same restrictions.  Errors: as sbvr_gemv_group; SBVR_ERR_SHAPE when a shard does not fit its M_full. */
+sbvr_status sbvr_gemv_group_to_peers(const sbvr_gemv_problem* probs, int32_t n, float* const* peer_y, int32_t n_peers,
+                                     const int32_t* y_row_offset, const int32_t* M_full, void* workspace,
+                                     size_t ws_bytes, void* stream);
+
 /* sbvr_gemv_ex -- as sbvr_gemv_batched with an explicit algorithm (sbvr_algo). */
 sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, float* Y, void* workspace,
                          size_t ws_bytes, int32_t algo, void* stream);

@@ -96,6 +96,9 @@ def lib():
             L.sbvr_gemv_chain.argtypes = [P, P, i32, P, P, sz, P, P]
         if hasattr(L, "sbvr_gemv_group"):
             L.sbvr_gemv_group.argtypes = [P, i32, P, sz, P]
+            if hasattr(L, "sbvr_gemv_group_to_peers"):
+                L.sbvr_gemv_group_to_peers.argtypes = [P, i32, P, i32, P, P, P, sz, P]
+                L.sbvr_gemv_group_to_peers.restype = i32
             L.sbvr_gemv_group_workspace_bytes.argtypes = [P, i32, P]
         if hasattr(L, "sbvr_gemv_to_peers"):
             L.sbvr_gemv_to_peers.argtypes = [P, P, i32, P, i32, i32, i32, P, sz, P]
@@ -437,6 +440,22 @@ def gemv_group(problems, ws: Optional[Workspace] = None):
     arr = _problems(problems)
     _check(lib().sbvr_gemv_group(arr, len(problems), _ptr(ws.buf), ws.nbytes, _stream()), "sbvr_gemv_group")
     return [y for (_, _, y) in problems]
+
+
+def gemv_group_to_peers(problems, peer_ptrs, y_row_offsets, M_fulls, ws: Optional[Workspace] = None) -> None:
+    """sbvr_gemv_group_to_peers: this rank's row-shard problems [(w, x), ...] in one grouped launch whose epilogue
+    stores problem i's y rows into every peer's full y of problem i (device pointers peer_ptrs[i][j], [M_fulls[i]]
+    fp32 each) at rows [y_row_offsets[i], + w.M)."""
+    n, n_peers = len(problems), len(peer_ptrs[0])
+    full = [(w, x, None) for (w, x) in problems]
+    if ws is None:
+        ws = group_workspace(full)
+    arr = _problems(full)
+    ptrs = (ctypes.c_void_p * (n * n_peers))(*[int(q) for row in peer_ptrs for q in row])
+    offs = (ctypes.c_int32 * n)(*[int(v) for v in y_row_offsets])
+    mf = (ctypes.c_int32 * n)(*[int(v) for v in M_fulls])
+    _check(lib().sbvr_gemv_group_to_peers(arr, n, ptrs, n_peers, offs, mf, _ptr(ws.buf), ws.nbytes, _stream()),
+           "sbvr_gemv_group_to_peers")
 
 
 def debug_partials(w: SbvrWeights, x: SbvrActivation, algo: int = ALGO_TC) -> torch.Tensor:

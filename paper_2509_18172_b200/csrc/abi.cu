@@ -388,6 +388,33 @@ sbvr_status sbvr_gemv_group_workspace_bytes(const sbvr_gemv_problem* probs, int3
   return SBVR_OK;
 }
 
+sbvr_status sbvr_gemv_group_to_peers(const sbvr_gemv_problem* probs, int32_t n, float* const* peer_y, int32_t n_peers,
+                                     const int32_t* y_row_offset, const int32_t* M_full, void* workspace,
+                                     size_t ws_bytes, void* stream) {
+  if (!peer_y || !y_row_offset || !M_full) return set_error(SBVR_ERR_INVALID_ARG, "peer_y / offsets / M_full is NULL");
+  if (n_peers < 1 || n_peers > 8) return set_error(SBVR_ERR_INVALID_ARG, "n_peers=%d outside 1..8", n_peers);
+  if (!probs || n < 1 || n > SBVR_GROUP_MAX) return set_error(SBVR_ERR_INVALID_ARG, "probs/n invalid");
+  // probs[i].y is not used: validate with a stand-in so check_group accepts the descriptors
+  sbvr_gemv_problem tmp[SBVR_GROUP_MAX];
+  for (int i = 0; i < n; ++i) {
+    tmp[i] = probs[i];
+    tmp[i].y = peer_y[i * n_peers];
+    if (y_row_offset[i] < 0 || M_full[i] < probs[i].w.M || y_row_offset[i] > M_full[i] - probs[i].w.M)
+      return set_error(SBVR_ERR_SHAPE, "problem %d: rows [%d, %d) do not fit M_full=%d", i, y_row_offset[i],
+                       y_row_offset[i] + probs[i].w.M, M_full[i]);
+    for (int j = 0; j < n_peers; ++j)
+      if (!peer_y[i * n_peers + j]) return set_error(SBVR_ERR_INVALID_ARG, "peer_y[%d][%d] is NULL", i, j);
+  }
+  sbvr_status s = check_group(tmp, n);
+  if (s != SBVR_OK) return s;
+  if (!workspace) return set_error(SBVR_ERR_WORKSPACE, "workspace is NULL");
+  GroupPeers gp;
+  gp.y = peer_y;
+  gp.n = n_peers;
+  gp.row_offset = y_row_offset;
+  return launch_gemv_group(tmp, n, workspace, ws_bytes, (cudaStream_t)stream, &gp);
+}
+
 sbvr_status sbvr_gemv_group(const sbvr_gemv_problem* probs, int32_t n, void* workspace, size_t ws_bytes, void* stream) {
   sbvr_status s = check_group(probs, n);
   if (s != SBVR_OK) return s;

@@ -32,6 +32,7 @@ namespace grp {
 using namespace mma;
 
 constexpr int kMaxProb = SBVR_GROUP_MAX;
+constexpr int kMaxPeers = 8;
 #ifndef SBVR_GROUP_WARPS
 #define SBVR_GROUP_WARPS 8
 #endif
@@ -60,7 +61,8 @@ struct GProb {
   const uint8_t* units;     // unit records of W_p (full 128-row blocks)
   const uint32_t* xplanes;  // [NG][l][4]
   const float* xscales;     // [NG]
-  float* Y;                 // [M]
+  float* Y[kMaxPeers];      // [M] -- or, fused all-gather (sbvr_gemv_group_to_peers), every rank's full y at this
+                            // rank's row offset (ny pointers)
   int NG;                   // groups per row
   int rbbase;               // first global row block of this problem
   int ubase;                // first global unit of this problem
@@ -71,6 +73,7 @@ struct GroupParams {
   const float* ratio_pow[kMaxProb];   // [n_ratio][K] per problem
   int n_ratio[kMaxProb];
   int np;                   // problems
+  int ny;                   // y destinations per problem (1; n_peers for the fused all-gather)
   int Us;                   // total units
   int C, qq, rr;            // CTAs and the unit partition over CTAs
   int l, one;
@@ -271,8 +274,12 @@ __global__ void __launch_bounds__(kGW * 32, kGC) gemv_group_kernel(GroupParams P
     const int row_a = 64 * hf + gq;                 // + 16 i' (i' = 0..3), + 8 for the second row of the lane
 
     float2 acc[4];
-  #pragma unroll
+#pragma unroll
     for (int i = 0; i < 4; ++i) acc[i] = make_float2(0.f, 0.f);
+    auto store_y = [&](int pp, int off, float v) {  // y row (local to problem pp) -> its destination(s)
+#pragma unroll 1
+      for (int j = 0; j < P.ny; ++j) P.pr[pp].Y[j][off] = v;
+    };
 
     // position of the current unit: problem p, global row block rb, group g (+ the problem's constants)
     int p = prob_of(P, U0);
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__(kGW * 32, kGC) gemv_group_kernel(GroupParams P
         }
       }
       const int cur_p = p, cur_rb = rb, cur_rat = rat_off;
-      float* const Ycur = P.pr[p].Y + 128 * (rb - rbb) + 64 * hf;
+      const int ycur = 128 * (rb - rbb) + 64 * hf;    // this warp's first y row of the unit's band
       const int ub0 = P.pr[p].ubase + (rb - rbb) * NGp;           // the row block's first and end global units
       const int ub1 = ub0 + NGp;
       // advance to the next unit (problem switch: reload the problem's constants)
@@ -452,7 +459,7 @@ __global__ void __launch_bounds__(kGW * 32, kGC) gemv_group_kernel(GroupParams P
           }
           if (!shared) {
   #pragma unroll
-            for (int h = 0; h < 2; ++h) Ycur[lane + 32 * h] = v[h];
+            for (int h = 0; h < 2; ++h) store_y(cur_p, ycur + lane + 32 * h, v[h]);
           } else {
             // last-arriver reduction over the CTAs holding units of the row block (deterministic CTA order; nobody
             // waits on another CTA's progress: see gemv_mma.cuh)
@@ -502,7 +509,7 @@ __global__ void __launch_bounds__(kGW * 32, kGC) gemv_group_kernel(GroupParams P
               }
               if (lane == 0) P.ws_cnt[b] = kSentinel;
   #pragma unroll
-              for (int h = 0; h < 2; ++h) Ycur[lane + 32 * h] = sum[h];
+              for (int h = 0; h < 2; ++h) store_y(cur_p, ycur + lane + 32 * h, sum[h]);
             }
           }
         }
@@ -626,7 +633,8 @@ size_t group_workspace_bytes(const sbvr_gemv_problem* pr, int n) {
   return grp::group_cnt_bytes(g) + group_part_bytes(g) + group_conv_bytes(group_xg(pr, n)) + 256;
 }
 
-sbvr_status launch_gemv_group(const sbvr_gemv_problem* pr, int n, void* ws, size_t ws_bytes, cudaStream_t st) {
+sbvr_status launch_gemv_group(const sbvr_gemv_problem* pr, int n, void* ws, size_t ws_bytes, cudaStream_t st,
+                              const GroupPeers* peers) {
   using namespace grp;
   const GroupPlan g = group_plan(pr, n);
   const size_t need = group_workspace_bytes(pr, n);
@@ -638,7 +646,7 @@ sbvr_status launch_gemv_group(const sbvr_gemv_problem* pr, int n, void* ws, size
     P.pr[i].units = pr[i].w.data;
     P.pr[i].xplanes = static_cast<const uint32_t*>(pr[i].x.data);
     P.pr[i].xscales = pr[i].x.scales;
-    P.pr[i].Y = pr[i].y;
+    P.pr[i].Y[0] = pr[i].y;
     P.pr[i].NG = pr[i].w.N / kG;
     P.pr[i].rbbase = rbs;
     P.pr[i].ubase = uu;
@@ -648,6 +656,12 @@ sbvr_status launch_gemv_group(const sbvr_gemv_problem* pr, int n, void* ws, size
     uu += (pr[i].w.M / 128) * (pr[i].w.N / kG);
   }
   P.np = n;
+  P.ny = 1;
+  if (peers) {                                     // fused all-gather: problem i's y rows -> every rank's full y
+    P.ny = peers->n;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < peers->n; ++j) P.pr[i].Y[j] = peers->y[i * peers->n + j] + peers->row_offset[i];
+  }
   P.Us = g.Us;
   P.C = g.C;
   P.qq = g.Us / g.C;

@@ -125,7 +125,13 @@ sbvr_status launch_gemv_zt(const sbvr_weights* w, const sbvr_act* x, int T, floa
                            int32_t* T_debug, cudaStream_t st);
 size_t zt_workspace_bytes(const sbvr_weights* w, int T);
 bool zt_supported(const sbvr_weights* w, const sbvr_act* x);
-sbvr_status launch_gemv_group(const sbvr_gemv_problem* pr, int n, void* ws, size_t ws_bytes, cudaStream_t st);
+struct GroupPeers {       // fused all-gather of a grouped GEMV: y[i * n + j] = rank j's full y of problem i
+  float* const* y;
+  int n;
+  const int32_t* row_offset;   // [problem] this rank's first row in the full y
+};
+sbvr_status launch_gemv_group(const sbvr_gemv_problem* pr, int n, void* ws, size_t ws_bytes, cudaStream_t st,
+                              const GroupPeers* peers = nullptr);
 size_t group_workspace_bytes(const sbvr_gemv_problem* pr, int n);
 sbvr_status launch_hadamard(const void* X, void* Y, int dtype, int rows, int N, int b, const int8_t* signs,
                             cudaStream_t st);

@@ -7,6 +7,7 @@ is NCCL (NVLink 5 / NVSwitch); the same host logic runs under gloo in the CPU te
 
 Two ways to join y:
 - `RowShardedGemv` (+ `sbvr_row_sharded`): the local GEMV, then an NCCL all-gather of the y shards;
+- `SymmGroupRowShardedGemv`: the same for several matrices in one grouped launch (a decoder layer's step);
 - `SymmRowShardedGemv`: the all-gather fused into the GEMV's epilogue -- every rank's kernel stores its y rows
   directly into every rank's full-y buffer in symmetric memory (torch.distributed._symmetric_memory: the same
   allocation mapped on all GPUs of the node, reached over NVLink 5 / NVSwitch), then one signal-pad barrier
@@ -103,6 +104,56 @@ class SymmRowShardedGemv:
         self.sb.gemv_to_peers(self.w, act, self.peer_ptrs, self.r0, self.M, self.ws)
         self.hdl.barrier(channel=0)
         return self.y_full if self.T > 1 else self.y_full[0]
+
+
+def group_peer_layout(M_fulls, world: int, rank: int):
+    """Layout of a grouped, row-sharded step: the full y of problem i lives at [base_i, base_i + M_fulls[i]) of one
+    flat buffer (the same on every rank); this rank writes its shard rows [r0_i, r1_i) of problem i.
+    Returns (base offsets, row offsets r0_i, shard rows r1_i - r0_i)."""
+    bases, r0s, rows, off = [], [], [], 0
+    for M in M_fulls:
+        r0, r1 = shard_range(M, world, rank)
+        bases.append(off)
+        r0s.append(r0)
+        rows.append(r1 - r0)
+        off += M
+    return bases, r0s, rows
+
+
+class SymmGroupRowShardedGemv:
+    """Several row-sharded GEMVs (e.g. a decoder layer's projections) as ONE grouped launch per rank whose epilogue
+    stores every y row into every rank's full y: one symmetric-memory buffer holds all problems' full y's
+    (group_peer_layout), rank p's sbvr_gemv_group_to_peers writes its shard rows of every problem into every rank's
+    copy through the peer pointers, then one signal-pad barrier orders the stores before anyone reads them.  No NCCL
+    call on the data path; capturable in a CUDA graph."""
+
+    def __init__(self, w_shards, M_fulls, group=None, ws: Optional[object] = None):
+        import paper_2509_18172_b200 as sb
+        import torch.distributed._symmetric_memory as symm_mem
+        self.sb = sb
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.M_fulls = list(M_fulls)
+        self.bases, self.r0s, rows = group_peer_layout(self.M_fulls, self.world, self.rank)
+        assert [w.M for w in w_shards] == rows
+        self.w = list(w_shards)
+        dev = w_shards[0].data.device
+        self.y_flat = symm_mem.empty((sum(self.M_fulls),), dtype=torch.float32, device=dev)
+        self.hdl = symm_mem.rendezvous(self.y_flat, self.group)
+        base_ptrs = [int(q) for q in self.hdl.buffer_ptrs]
+        assert len(base_ptrs) == self.world
+        self.peer_ptrs = [[bp + 4 * b for bp in base_ptrs] for b in self.bases]
+        self.ws = ws
+        self.y_full = [self.y_flat[b:b + M] for b, M in zip(self.bases, self.M_fulls)]
+
+    def __call__(self, acts):
+        probs = list(zip(self.w, acts))
+        if self.ws is None:
+            self.ws = self.sb.group_workspace([(w, a, None) for w, a in probs])
+        self.sb.gemv_group_to_peers(probs, self.peer_ptrs, self.r0s, self.M_fulls, self.ws)
+        self.hdl.barrier(channel=0)
+        return self.y_full
 
 
 def encode_shard(W_full: torch.Tensor, world: int, rank: int, **kw):

@@ -120,3 +120,49 @@ def test_fused_epilogue_addressing_gloo_world3():
     for p in procs:
         p.join(timeout=60)
     assert sorted(r[0] for r in res) == [0, 1, 2] and all(r[1] for r in res), res
+
+
+def _group_peer_worker(rank, world, port, shared, q):
+    """The grouped fused epilogue's addressing (dist.group_peer_layout, what SymmGroupRowShardedGemv hands to
+    sbvr_gemv_group_to_peers): every rank writes its shard rows of several problems into ONE shared flat buffer
+    of all problems' full y's; after the barrier it must equal the unsharded oracle y of every problem."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import synthetic
+        from paper_2509_18172_b200.dist import group_peer_layout
+        mats = [(96, 256), (48, 128), (144, 384)]
+        bases, r0s, rows = group_peer_layout([M for M, _ in mats], world, rank)
+        fulls = []
+        for i, (M, N) in enumerate(mats):
+            pc, s16, b16, ri = synthetic.random_encoded(M, N, 4, 16, seed=20 + i)
+            x = synthetic.activation(N, seed=30 + i)[0]
+            z, xp, sc = oracle.encode_vector(x, 128, 8)
+            xd = oracle.x_dec_sbvr(z, sc)
+            r0, r1 = r0s[i], r0s[i] + rows[i]
+            enc = oracle.Encoded(r1 - r0, N, oracle.OracleConfig(K=4), pc[r0:r1].copy(), s16[r0:r1].copy(),
+                                 b16[r0:r1].copy(), ri[r0:r1].copy(), None)
+            shared[bases[i] + r0:bases[i] + r1] = torch.from_numpy(oracle.gemv_rows(enc, xd))
+            fulls.append(oracle.gemv_rows(oracle.Encoded(M, N, oracle.OracleConfig(K=4), pc, s16, b16, ri, None), xd))
+        dist.barrier()
+        ok = all(np.array_equal(shared[b:b + M].numpy(), f) for b, (M, _), f in zip(bases, mats, fulls))
+        q.put((rank, bool(ok and bases == [0, 96, 144])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_grouped_fused_epilogue_addressing_gloo_world3():
+    world = 3
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    shared = torch.full((96 + 48 + 144,), float("nan"), dtype=torch.float64).share_memory_()
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_group_peer_worker, args=(r, world, port, shared, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(r[0] for r in res) == [0, 1, 2] and all(r[1] for r in res), res

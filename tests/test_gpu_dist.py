@@ -97,3 +97,63 @@ def test_symmetric_memory_world1_matches_gemv():
         assert torch.equal(g.y_full[0], ref)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gemv_group_to_peers_offsets_and_values(world):
+    """Every rank's grouped shard launch (simulated rank by rank on the one GPU) stores each problem's rows at its
+    offset in every peer buffer; bit-identical to sbvr_gemv_group of the same shard problems; nothing else written."""
+    mats = [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)]
+    n_peers = 3
+    fulls = [[torch.full((M,), float("nan"), device=DEV) for (M, _) in mats] for _ in range(n_peers)]
+    ptrs = [[fulls[j][i].data_ptr() for j in range(n_peers)] for i in range(len(mats))]
+    refs = []
+    for rank in range(world):
+        bases, r0s, rows = sdist.group_peer_layout([M for M, _ in mats], world, rank)
+        probs = []
+        for i, (M, N) in enumerate(mats):
+            pc, s16, b16, ri = synthetic.random_encoded(rows[i], N, 4, 16, seed=100 * rank + i)
+            w = sb.pack_canonical(pc, s16, b16, ri, 16)
+            act = sb.encode_vector(torch.from_numpy(synthetic.activation(N, seed=7 + i)).to(DEV))
+            probs.append((w, act))
+        sb.gemv_group_to_peers(probs, ptrs, r0s, [M for M, _ in mats])
+        ys = sb.gemv_group([(w, a, None) for w, a in probs])
+        refs.append((r0s, rows, ys))
+    torch.cuda.synchronize()
+    for j in range(n_peers):
+        for r0s, rows, ys in refs:
+            for i in range(len(mats)):
+                assert torch.equal(fulls[j][i][r0s[i]:r0s[i] + rows[i]], ys[i])
+        assert not any(torch.isnan(f).any() for f in fulls[j])
+
+
+def test_symmetric_memory_world1_grouped_matches_group():
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV, 0))
+    try:
+        mats = [(6144, 4096), (4096, 4096), (28672, 4096), (4096, 14336)]
+        ws_, acts = [], []
+        for i, (M, N) in enumerate(mats):
+            pc, s16, b16, ri = synthetic.random_encoded(M, N, 4, 16, seed=50 + i)
+            ws_.append(sb.pack_canonical(pc, s16, b16, ri, 16))
+            acts.append(sb.encode_vector(torch.from_numpy(synthetic.activation(N, seed=60 + i)).to(DEV)))
+        g = sdist.SymmGroupRowShardedGemv(ws_, [M for M, _ in mats])
+        ys = [y.clone() for y in g(acts)]
+        refs = sb.gemv_group([(w, a, None) for w, a in zip(ws_, acts)])
+        torch.cuda.synchronize()
+        assert all(torch.equal(y, r) for y, r in zip(ys, refs))
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            g(acts)
+            torch.cuda.synchronize()
+            cg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(cg, stream=st):
+                g(acts)
+            g.y_flat.fill_(float("nan"))
+            cg.replay()
+        torch.cuda.synchronize()
+        assert all(torch.equal(y, r) for y, r in zip(g.y_full, refs))
+    finally:
+        dist.destroy_process_group()
