@@ -1106,7 +1106,11 @@ def main():
                             f"{res['ev_every']}th); traffic = ncu dram "
                             "read+write bytes per launch (profiles/" + TRAFFIC_FILE[args.step] + ")",
                      "gemv_span_us": round(res["span_ms_avg"] * 1e3, 3),
-                     "algorithmic_bytes_per_launch": round(tot_b / n_launch_gemv)},
+                     "algorithmic_bytes_per_launch": round(tot_b / n_launch_gemv),
+                     # (the event nodes around the measured launches cut their programmatic overlap with the
+                     # neighbouring launches, so `achieved` is conservative; the same bytes over the steady-state step)
+                     "achieved_steady_state": round(tot_b / (ms_per_step * 1e-3) / 1e9, 1),
+                     "frac_steady_state": round(tot_b / (ms_per_step * 1e-3) / 1e9 / peak, 4)},
         "per_gemv": per,
         "per_gemv_how": "diagnostic after the timed region: event nodes between the 4 launches (no launch "
                         "overlap), so each figure includes a full launch + ramp",
