@@ -450,7 +450,9 @@ def run_sbvr(args, world, rank, local_rank, pg):
         # sync on both sides; an event after every replay
         n_multi, n_single = args.steps // spg, args.steps % spg
         span_ms, span_n = 0.0, 0
-        ev_every = min(EV_EVERY, max(1, n_multi // 4))   # short runs (--steps 20) still get span samples
+        # one replay in ev_every carries the span events (at most a quarter of them: the event nodes cut the
+        # programmatic overlap around that step); a run too short for any gets one instrumented replay afterwards
+        ev_every = min(EV_EVERY, max(4, n_multi // 4))
         pending = {}
         if world > 1:
             torch.distributed.barrier(group=pg)
@@ -477,9 +479,14 @@ def run_sbvr(args, world, rank, local_rank, pg):
         for gi in pending:
             span_ms += cr.elapsed_ms(*ev_graphs[gi][1])
             span_n += 1
+        elapsed = evs[0].elapsed_time(evs[-1])
+        if span_n == 0:                                 # (after the timed region: not part of `elapsed`)
+            ev_graphs[0][0].replay()
+            torch.cuda.synchronize()
+            span_ms += cr.elapsed_ms(*ev_graphs[0][1])
+            span_n += 1
         if world > 1:
             torch.distributed.barrier(group=pg)
-        elapsed = evs[0].elapsed_time(evs[-1])
         step_ms = ([evs[i].elapsed_time(evs[i + 1]) / spg for i in range(n_multi)] +
                    [evs[n_multi + i].elapsed_time(evs[n_multi + i + 1]) for i in range(n_single)])
         clocks = sampler.summary(wall_heat, wall1) if sampler else None
