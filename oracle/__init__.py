@@ -84,6 +84,8 @@ def lib():
         L.oracle_partials_rows.argtypes = [P, P, P, i32, i32, i32, i32, P, i32, P, P]
         L.oracle_max_threads.restype = i32
         L.oracle_hadamard_rows.argtypes = [P, P, i32, i32, i32, P]
+        L.oracle_prefill_decode_fp16.argtypes = [P, P, P, P, i32, i32, i32, i32, i32, P]
+        L.oracle_prefill_rows.argtypes = [P, P, P, P, i32, i32, i32, i32, i32, P, i32, P, i32, P]
         L.oracle_entry_mse.restype = f64
         L.oracle_entry_mse.argtypes = [P, i32, i32, f64, f64, f64]
         L.oracle_encode_matrix_cached.restype = i32
@@ -242,6 +244,25 @@ def gemv_rows(enc: Encoded, x_dec, rows=None) -> np.ndarray:
     lib().oracle_gemv_rows(_p(enc.planes), _p(enc.s16), _p(enc.b16), _p(enc.r_idx), enc.M, enc.N, enc.cfg.K,
                            enc.cfg.group_size, enc.cfg.n_ratio, _p(x_dec), _p(rows), len(rows), _p(y))
     return y
+
+
+def prefill_decode(enc: Encoded) -> np.ndarray:
+    """O-PF decode (§5.1, reading A25): the FP16 decompressed weights [M][N] as uint16 bit patterns."""
+    W16 = np.zeros((enc.M, enc.N), np.uint16)
+    lib().oracle_prefill_decode_fp16(_p(enc.planes), _p(enc.s16), _p(enc.b16), _p(enc.r_idx), enc.M, enc.N,
+                                     enc.cfg.K, enc.cfg.group_size, enc.cfg.n_ratio, _p(W16))
+    return W16
+
+
+def prefill_rows(enc: Encoded, X16, rows=None) -> np.ndarray:
+    """O-PF GEMM: Y[tau][i] = sum_e w16[rows[i], e] x16[tau, e] in fp64; X16 fp16 [T][N]."""
+    X16 = np.ascontiguousarray(np.asarray(X16, np.float16).reshape(-1, enc.N)).view(np.uint16)
+    rows = np.arange(enc.M, dtype=np.int32) if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
+    T = X16.shape[0]
+    Y = np.zeros((T, len(rows)), np.float64)
+    lib().oracle_prefill_rows(_p(enc.planes), _p(enc.s16), _p(enc.b16), _p(enc.r_idx), enc.M, enc.N, enc.cfg.K,
+                              enc.cfg.group_size, enc.cfg.n_ratio, _p(X16), T, _p(rows), len(rows), _p(Y))
+    return Y
 
 
 def x_dec_fp16(x16) -> np.ndarray:

@@ -559,3 +559,73 @@ void oracle_hadamard_rows(const double* X, double* Y, int rows, int N, int b, co
     }
   }
 }
+
+/* ------------------------------------------------------------------ O-PF prefill: FP16 decompression + GEMM
+ * PAPER.md P:279 (§5.1): "we design a prefill kernel that decompresses SBVR weights into FP16 and transfers
+ * the recovered weight segments to tensor cores for GEMM computation".  The paper does not say how the FP16
+ * value is formed; reading A25: the coefficients of Eq. 4 are formed in fp32,
+ *     c32_t = fmaf(s, (float) r^t, b)        (r^t by repeated fp64 multiplication, as oracle_coefficients)
+ * rounded to fp16 (c16_t, round to nearest even), and the element is summed in fp16 arithmetic in plane order,
+ *     w16 = fl16( ... fl16(fl16(0 + beta_0 c16_0) + beta_1 c16_1) ... + beta_{K-1} c16_{K-1})
+ * (each partial sum of two fp16 values is exact in fp64 and rounded once).  The GEMM is the plain definition
+ * y[tau][r] = sum_e fp64(w16[r][e]) * fp64(x16[tau][e]), e increasing, fp64.                                */
+static void prefill_coefs16(double r, uint16_t s16, uint16_t b16, int K, double* c16) {
+  const float s = (float)oracle_fp16_to_double(s16), b = (float)oracle_fp16_to_double(b16);
+  double p = 1.0;
+  for (int t = 0; t < K; ++t) {
+    const float c32 = fmaf(s, (float)p, b);
+    c16[t] = oracle_fp16_to_double(oracle_fp16_bits((double)c32));
+    p = p * r;
+  }
+}
+
+static uint16_t prefill_element16(const uint32_t* pl, int WPG, int e, const double* c16, int K) {
+  double acc = 0.0;
+  for (int t = 0; t < K; ++t)
+    if ((pl[t * WPG + e / 32] >> (e % 32)) & 1u) acc = oracle_fp16_to_double(oracle_fp16_bits(acc + c16[t]));
+  return oracle_fp16_bits(acc);
+}
+
+void oracle_prefill_decode_fp16(const uint32_t* planes, const uint16_t* s16, const uint16_t* b16,
+                                const uint8_t* r_idx, int M, int N, int K, int G, int n_ratio, uint16_t* W16) {
+  const int NG = N / G, WPG = G / 32;
+  double R[256];
+  oracle_ratio_set(n_ratio, R);
+  for (long q = 0; q < (long)M * NG; ++q) {
+    const long r = q / NG, g = q % NG;
+    double c16[OR_MAX_K];
+    prefill_coefs16(R[r_idx[q]], s16[q], b16[q], K, c16);
+    const uint32_t* pl = planes + q * (long)K * WPG;
+    for (int e = 0; e < G; ++e) W16[r * (long)N + g * G + e] = prefill_element16(pl, WPG, e, c16, K);
+  }
+}
+
+void oracle_prefill_rows(const uint32_t* planes, const uint16_t* s16, const uint16_t* b16, const uint8_t* r_idx,
+                         int M, int N, int K, int G, int n_ratio, const uint16_t* X16, int T, const int32_t* row_ids,
+                         int n_rows, double* Y) {
+  const int NG = N / G, WPG = G / 32;
+  double R[256];
+  oracle_ratio_set(n_ratio, R);
+  (void)M;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+  for (int i = 0; i < n_rows; ++i) {
+    const long r = row_ids[i];
+    double* w = (double*)malloc(sizeof(double) * (size_t)N);
+    for (int g = 0; g < NG; ++g) {
+      const long q = r * NG + g;
+      double c16[OR_MAX_K];
+      prefill_coefs16(R[r_idx[q]], s16[q], b16[q], K, c16);
+      const uint32_t* pl = planes + q * (long)K * WPG;
+      for (int e = 0; e < G; ++e) w[g * G + e] = oracle_fp16_to_double(prefill_element16(pl, WPG, e, c16, K));
+    }
+    for (int tau = 0; tau < T; ++tau) {
+      const uint16_t* x = X16 + (size_t)tau * N;
+      double acc = 0.0;
+      for (int e = 0; e < N; ++e) acc = acc + w[e] * oracle_fp16_to_double(x[e]);
+      Y[(size_t)tau * n_rows + i] = acc;
+    }
+    free(w);
+  }
+}
