@@ -293,6 +293,24 @@ sbvr_status sbvr_gemv_ex(const sbvr_weights* w, const sbvr_act* X, int32_t T, fl
  * Buffers 16-byte aligned. */
 sbvr_status sbvr_hadamard_rows(const void* X, void* Y, int32_t dtype, int32_t rows, int32_t N, int32_t block,
                                const int8_t* signs, void* stream);
+/* sbvr_prefill -- the prefill GEMM of PAPER.md P:279 (§5.1): "a prefill kernel that decompresses SBVR
+ * weights into FP16 and transfers the recovered weight segments to tensor cores for GEMM computation".
+ *   Y[tau][r] = sum_e w16[r][e] * X[tau][e]      (fp32 accumulation on tcgen05.mma kind::f16)
+ * with w16 the FP16 decompression of reading A25: c16_t = fp16(fmaf(s, r^t, b)) and
+ * w16 = fl16(... fl16(beta_0 c16_0) + ... + beta_{K-1} c16_{K-1}) in plane order -- bit-identical to the
+ * oracle's O-PF decode.  One pass over the weights per 256 tokens.
+ *   w          SBVR_META_GROUP weights, K = 1..4, any M (multiple of 16), N multiple of 128 (device)
+ *   X          device, fp16 bit patterns [T][N] row-major (2-byte aligned); read-only
+ *   T          tokens, >= 0 (0: nothing enqueued); any size (passes of 256)
+ *   Y          device, fp32 [T][M] row-major (4-byte aligned); every element written
+ *   workspace  device, 256-byte aligned, >= sbvr_prefill_workspace_bytes(w, T); initialised once with
+ *              sbvr_workspace_init and left at rest by every call (the token relayout scratch inside it is
+ *              overwritten); one call at a time per workspace.
+ * Errors: SBVR_ERR_UNSUPPORTED (indexed meta, K > 4), _SHAPE (T < 0), _ALIGNMENT, _WORKSPACE, _CUDA. */
+sbvr_status sbvr_prefill_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* bytes);
+sbvr_status sbvr_prefill(const sbvr_weights* w, const uint16_t* X, int32_t T, float* Y, void* workspace,
+                         size_t ws_bytes, void* stream);
+
 /* Test-only: the integer popcount partials P[m][g][t][j] = popc(beta_t & d_j) over the group,
  * int32 [M][N/G][K][l] row-major (device), computed by the kernel `algo` (POPC, TC or MMA) from an
  * SBVR-x activation (T = 1). */

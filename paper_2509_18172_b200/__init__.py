@@ -100,6 +100,9 @@ def lib():
                 L.sbvr_gemv_group_to_peers.argtypes = [P, i32, P, i32, P, P, P, sz, P]
                 L.sbvr_gemv_group_to_peers.restype = i32
             L.sbvr_gemv_group_workspace_bytes.argtypes = [P, i32, P]
+        if hasattr(L, "sbvr_prefill"):
+            L.sbvr_prefill.argtypes = [P, P, i32, P, P, sz, P]
+            L.sbvr_prefill_workspace_bytes.argtypes = [P, i32, P]
         if hasattr(L, "sbvr_gemv_to_peers"):
             L.sbvr_gemv_to_peers.argtypes = [P, P, i32, P, i32, i32, i32, P, sz, P]
         # (A/B timing loads older builds through SBVR_LIB_AB: symbols they lack are simply not declared)
@@ -108,7 +111,7 @@ def lib():
                      "sbvr_pack_canonical", "sbvr_unpack_canonical", "sbvr_fill_ratio_table", "sbvr_hadamard_rows", "sbvr_encode_weights_cached",
                      "sbvr_debug_zt_sums", "sbvr_gemv_to_peers", "sbvr_weights_bytes_ex",
                      "sbvr_encode_weights_indexed", "sbvr_pack_indexed", "sbvr_unpack_indexed", "sbvr_gemv_chain",
-                     "sbvr_gemv_group", "sbvr_gemv_group_workspace_bytes"):
+                     "sbvr_gemv_group", "sbvr_gemv_group_workspace_bytes", "sbvr_prefill", "sbvr_prefill_workspace_bytes"):
             if hasattr(L, name):
                 getattr(L, name).restype = i32
         _lib = L
@@ -404,6 +407,31 @@ def gemv_to_peers(w: SbvrWeights, x: SbvrActivation, peer_ptrs, y_row_offset: in
     wd, xd = w.desc(), x.desc()
     _check(lib().sbvr_gemv_to_peers(ctypes.byref(wd), ctypes.byref(xd), x.T, arr, len(peer_ptrs), int(y_row_offset),
                                     int(M_full), _ptr(ws.buf), ws.nbytes, _stream()), "sbvr_gemv_to_peers")
+
+
+def prefill_workspace(w: SbvrWeights, T: int) -> Workspace:
+    n = ctypes.c_size_t()
+    d = w.desc()
+    _check(lib().sbvr_prefill_workspace_bytes(ctypes.byref(d), int(T), ctypes.byref(n)), "sbvr_prefill_workspace_bytes")
+    return Workspace(n.value, w.data.device)
+
+
+def prefill(w: SbvrWeights, X: torch.Tensor, Y: Optional[torch.Tensor] = None,
+            ws: Optional[Workspace] = None) -> torch.Tensor:
+    """sbvr_prefill (§5.1): Y[T, M] = w16 X^T with the weights decompressed to FP16 (reading A25) and the
+    GEMM on tcgen05 kind::f16; X fp16 [T, N] on the device."""
+    assert X.is_cuda and X.dtype == torch.float16 and X.is_contiguous()
+    X2 = X.view(1, -1) if X.dim() == 1 else X
+    T = X2.shape[0]
+    assert X2.shape[1] == w.N
+    if Y is None:
+        Y = torch.empty((T, w.M), dtype=torch.float32, device=w.data.device)
+    if ws is None:
+        ws = prefill_workspace(w, T)
+    wd = w.desc()
+    _check(lib().sbvr_prefill(ctypes.byref(wd), _ptr(X2), T, _ptr(Y), _ptr(ws.buf), ws.nbytes, _stream()),
+           "sbvr_prefill")
+    return Y
 
 
 GROUP_MAX = 8

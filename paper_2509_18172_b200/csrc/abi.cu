@@ -457,6 +457,37 @@ sbvr_status sbvr_debug_partials(const sbvr_weights* w, const sbvr_act* x, int32_
   return set_error(SBVR_ERR_INVALID_ARG, "bad algo %d", algo);
 }
 
+static sbvr_status check_prefill(const sbvr_weights* w, int32_t T) {
+  sbvr_status s = check_weights(w);
+  if (s != SBVR_OK) return s;
+  if (w->meta_kind != SBVR_META_GROUP)
+    return set_error(SBVR_ERR_UNSUPPORTED, "prefill reads SBVR_META_GROUP weights (decompress indexed weights' table)");
+  if (w->K < 1 || w->K > 4) return set_error(SBVR_ERR_UNSUPPORTED, "prefill: K=%d (1..4)", w->K);
+  if (T < 0) return set_error(SBVR_ERR_SHAPE, "T=%d", T);
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_prefill_workspace_bytes(const sbvr_weights* w, int32_t T, size_t* bytes) {
+  sbvr_status s = check_prefill(w, T);
+  if (s != SBVR_OK) return s;
+  if (!bytes) return set_error(SBVR_ERR_INVALID_ARG, "bytes is NULL");
+  *bytes = T > 0 ? prefill_workspace_bytes(w, T) : 0;
+  return SBVR_OK;
+}
+
+sbvr_status sbvr_prefill(const sbvr_weights* w, const uint16_t* X, int32_t T, float* Y, void* workspace,
+                         size_t ws_bytes, void* stream) {
+  sbvr_status s = check_prefill(w, T);
+  if (s != SBVR_OK) return s;
+  if (T == 0) return SBVR_OK;
+  if (!X || !Y) return set_error(SBVR_ERR_INVALID_ARG, "X or Y is NULL");
+  if ((reinterpret_cast<uintptr_t>(X) & 1) || (reinterpret_cast<uintptr_t>(Y) & 3))
+    return set_error(SBVR_ERR_ALIGNMENT, "X must be 2-byte and Y 4-byte aligned");
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255))
+    return set_error(workspace ? SBVR_ERR_ALIGNMENT : SBVR_ERR_WORKSPACE, "workspace NULL or not 256-byte aligned");
+  return launch_prefill(w, X, T, Y, workspace, ws_bytes, (cudaStream_t)stream);
+}
+
 sbvr_status sbvr_debug_zt_sums(const sbvr_weights* w, const sbvr_act* x, int32_t T, int32_t* Tsum, void* stream) {
   sbvr_status s = check_weights(w);
   if (s != SBVR_OK) return s;

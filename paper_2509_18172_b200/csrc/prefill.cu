@@ -1,0 +1,629 @@
+// prefill.cu -- SBVR prefill GEMM on the 5th-generation tensor cores: PAPER.md P:279 (§5.1), "we design a
+// prefill kernel that decompresses SBVR weights into FP16 and transfers the recovered weight segments to
+// tensor cores for GEMM computation".  Y[tau][r] = sum_e w16[r][e] x16[tau][e], fp32
+// accumulation, for T fp16 tokens: every weight unit record is read from HBM and decompressed once per pass
+// of up to 256 tokens, and the per-(row, group) coefficients are applied before the MMA, so one accumulator
+// runs over the whole inner dimension (no per-group epilogue, unlike the z-column kernel gemv_zt.cu).
+//
+// FP16 decompression (reading A25; the oracle's O-PF):
+//     c16_t = fp16(fmaf(s, r^t, b)),   w16 = fl16(...fl16(beta_0 c16_0) + beta_1 c16_1 ... + beta_{K-1} c16_{K-1})
+// evaluated two elements at a time with HFMA2.  A plane bit becomes an exact fp16 power of two by masking
+// it into the exponent field: after shifting the plane word so that elements j and j + 16 sit at bits 12
+// and 28 (and j + 1, j + 17 at 13 and 29), `word & 0x10001000` is the half2 (beta_j, beta_{j+16}) * 2^-11 and
+// `word & 0x20002000` the pair (beta_{j+1}, beta_{j+17}) * 2^-7; the HFMA2 coefficient is c16 * 2^11 (resp.
+// 2^7), so the product is exactly beta * c16 and each HFMA2 rounds once, as the reading says.  One rotation,
+// two LOP3 and two HFMA2 per four elements and plane (the shift as an IMAD on the FMA pipe, balancing the ALU pipe).  (|c16| >= 32 would overflow c16 * 2^11: such a row
+// group takes a bit-select path with the same HFMA2 sequence instead.)  The A columns therefore hold the
+// element pairs (j, j + 16) of each 32-element word; the pre-pass lays the tokens out in the same K order.
+//
+// CTA = one SM, persistent over a balanced contiguous range of (128-row block, group) units (the records of
+// include/sbvr.h), 25 warps:
+//   warps 0..15   decompression, thread = row = TMEM lane; two groups of 8 warps take alternate units; warp w:
+//                 lane quarter w % 4, words 2h, 2h + 1 (h = (w / 4) % 2): K plane words -> 32 half2 columns ->
+//                 tcgen05.st into a 4-slot A ring in tensor memory
+//   warp 16..19   epilogue, thread = row: at the end of each row-block segment tcgen05.ld of D -> Y, or the
+//                 CTA's partial to the workspace + last-arriver combine (deterministic, as gemv_zt.cu)
+//   warps 20..23  MMA issuers: 8 x tcgen05.mma kind::f16 (M = 128, N = NT, K = 16) per unit, A from TMEM,
+//                 B (the tokens' group slice, canonical K-major layout) from shared memory; up to 4 issuers
+//                 split the 8 K-slices, each into its own accumulator, summed in order by the epilogue
+//   warp 24       producer: cp.async.bulk of the unit record and of the tokens' group slice into an S-stage ring
+#include <cstdlib>
+
+#include "ptx_sm100.cuh"
+#include "sbvr_internal.cuh"
+
+namespace sbvr {
+namespace pf {
+
+using namespace ptx;
+
+constexpr int kDeqWarps = 16;
+constexpr int kEpiWarps = 4;
+constexpr int kIssuerWarp = kDeqWarps + kEpiWarps;   // first of 4 issuer warps (one per SM sub-partition)
+constexpr int kProducerWarp = kIssuerWarp + 4;
+constexpr int kThreads = (kProducerWarp + 1) * 32;
+constexpr int kAS = 4;              // A slots (units in flight between decompression and MMA; a power of 2)
+constexpr int kMaxNT = 256;         // tokens per weight pass (MMA N)
+constexpr int kMaxPlanes = 4;
+constexpr int kSmemBudget = 220 * 1024;
+constexpr unsigned int kSentinel = 0xFFFFFFFFu;
+#ifndef PF_MIN_UNITS
+#define PF_MIN_UNITS 8
+#endif
+
+struct PfParams {
+  const uint8_t* units;     // unit records (sbvr.h)
+  const float* ratio_pow;   // [n_ratio][K]
+  const uint8_t* xc;        // this pass: [NG][NT x 128 fp16 in the B layout below]
+  float* Y;                 // this pass: [ntok][M]
+  float* ws_part;           // [CTA][2 (first / last row block)][NT][128]
+  unsigned int* ws_cnt;     // [row block] arrival counters (0xFFFFFFFF at rest)
+  int M, N, n_ratio, ntok;
+  int n_full, tail_rows;
+  int Us, qq, rr;
+  unsigned long long* ts;   // diagnostics (-DSBVR_DIAG, env SBVR_TS_PTR): [CTA][32] per-phase SM-cycle totals
+};
+#ifdef SBVR_DIAG
+#define PH_DECL unsigned long long ph_[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long ph_last_ = clock64();
+#define PH(s) do { const long long n_ = clock64(); ph_[s] += n_ - ph_last_; ph_last_ = n_; } while (0)
+#define PH_DUMP(base) do { if (p.ts && lane == 0) for (int i_ = 0; i_ < 8; ++i_) \
+                             p.ts[(size_t)blockIdx.x * 32 + (base) + i_] = ph_[i_]; } while (0)
+#else
+#define PH_DECL
+#define PH(s) do { } while (0)
+#define PH_DUMP(base) do { } while (0)
+#endif
+
+__device__ __forceinline__ int range_begin(int c, int qq, int rr) { return c * qq + min(c, rr); }
+__device__ __forceinline__ int unit_cta(int v, int qq, int rr) {
+  const int big = rr * (qq + 1);
+  return v < big ? v / (qq + 1) : rr + (v - big) / qq;
+}
+
+// K order of a group inside the MMA (A columns and the B rows agree on it): MMA k index kk = 2 col + h,
+// col = 16 c + j  ->  element 32 c + j + 16 h
+__host__ __device__ __forceinline__ int k_to_elem(int kk) {
+  const int col = kk >> 1, h = kk & 1;
+  return 32 * (col >> 4) + (col & 15) + 16 * h;
+}
+
+template <int NT>
+struct Geo {
+  static constexpr int kBBytes = NT * 128 * 2;            // one group's B tile (NT tokens x 128 fp16)
+  // MMA issuers: a small-N tcgen05.mma holds its issuing thread for ~50-150 cycles, so up to 4 warps issue the 8
+  // K-slices of a unit, each into its own accumulator D_i (summed by the epilogue in issuer order: deterministic)
+  static constexpr int kIss = NT <= 64 ? 4 : NT == 128 ? 2 : 1;
+  static constexpr int kQ = 8 / kIss;                    // MMAs per issuer per unit
+  static constexpr int kDB = 2 * kIss * NT <= 256 ? 2 : 1;   // D buffers (double-buffered when they fit)
+  static constexpr int kACol = kDB * kIss * NT;          // first A-slot column
+  static_assert(kACol + kAS * 64 <= 512, "tensor memory");
+  static constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(NT >> 3) << 17) | (8u << 24);   // f32 += f16 * f16
+};
+
+// ------------------------------------------------------------------ token relayout (pre-pass)
+// xc[pass][g][q][ng][kh][r][i] = X[256 pass + 8 ng + r][128 g + k_to_elem(16 q + 8 kh + i)], zero past T:
+// per MMA q a [NT/8][2][8][8] block = the canonical no-swizzle K-major layout (core matrices of 8 rows x
+// 16 B, LBO = 128 B between the K halves, SBO = 256 B between 8-row groups).  One thread per 16-byte row.
+__global__ void pf_relayout_kernel(const uint16_t* X, int T, int N, int NT, int passes, uint8_t* xc) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int NG = N / kG;
+  const long per_group = (long)NT * 16;                  // 16-byte rows per group tile
+  const long total = (long)passes * NG * per_group;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const long pg = idx / per_group;
+    int rem = (int)(idx - pg * per_group);
+    const int pass = (int)(pg / NG), g = (int)(pg % NG);
+    const int q = rem / (NT * 2);
+    rem -= q * NT * 2;
+    const int ng = rem >> 4, kh = (rem >> 3) & 1, r = rem & 7;
+    const int tok = pass * kMaxNT + 8 * ng + r;
+    uint32_t v[4] = {0u, 0u, 0u, 0u};
+    if (tok < T) {
+      const uint16_t* row = X + (size_t)tok * N + (size_t)g * kG;
+#pragma unroll
+      for (int i2 = 0; i2 < 4; ++i2) {
+        const int kk = 16 * q + 8 * kh + 2 * i2;
+        v[i2] = (uint32_t)__ldg(row + k_to_elem(kk)) | ((uint32_t)__ldg(row + k_to_elem(kk + 1)) << 16);
+      }
+    }
+    *reinterpret_cast<uint4*>(xc + (size_t)idx * 16) = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+}
+
+// w << sh (sh >= 0) or w >> -sh, on the FMA pipe (IMAD / IMAD.HI by a power of two): the masks that follow run on
+// the ALU pipe, the HFMA2s on the FMA pipe.  Bits shifted out are never selected by the masks.
+__device__ __forceinline__ uint32_t rot_fma(uint32_t w, int sh) {
+  uint32_t r;
+  if (sh == 0) return w;
+  if (sh > 0) asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(1u << sh));
+  else asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(1u << (32 + sh)));
+  return r;
+}
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 bits_h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+
+// ------------------------------------------------------------------ main kernel
+template <int K, int NT>
+__global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S) {
+  static_assert(K >= 1 && K <= kMaxPlanes, "K");
+  using GE = Geo<NT>;
+  constexpr int kUnitFull = 128 * (16 * K + 5);
+  constexpr int kUnitSlot = (kUnitFull + 127) / 128 * 128;
+  constexpr int kStage = kUnitSlot + GE::kBBytes;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ float s_rpow[64 * kMaxPlanes];
+  __shared__ __align__(8) uint64_t bar_full[8];
+  __shared__ __align__(8) uint64_t bar_empty[8];
+  __shared__ __align__(8) uint64_t bar_afull[kAS];
+  __shared__ __align__(8) uint64_t bar_afree[kAS];
+  __shared__ __align__(8) uint64_t bar_dfull[2];
+  __shared__ __align__(8) uint64_t bar_dempty[2];
+  __shared__ uint32_t s_tmem;
+  __shared__ unsigned int s_old;
+
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NG = p.N / kG;
+  const int cta = blockIdx.x;
+  const int V0 = range_begin(cta, p.qq, p.rr);
+  const int V1 = range_begin(cta + 1, p.qq, p.rr);
+  const int n = V1 - V0;
+  const long full_units = (long)p.n_full * NG;
+  const uint32_t tail_ub = (uint32_t)p.tail_rows * (16 * K + 5);
+  auto unit_src = [&](int u) -> const uint8_t* {
+    return u < full_units ? p.units + (size_t)u * kUnitFull
+                          : p.units + (size_t)full_units * kUnitFull + (size_t)(u - full_units) * tail_ub;
+  };
+  auto unit_bytes = [&](int u) -> uint32_t { return u < full_units ? (uint32_t)kUnitFull : tail_ub; };
+  auto rows_of = [&](int rb) { return rb < p.n_full ? 128 : p.tail_rows; };
+
+  if (tid == kProducerWarp * 32) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], kDeqWarps / 2 + GE::kIss);
+    }
+    for (int a = 0; a < kAS; ++a) {
+      mbar_init(&bar_afull[a], kDeqWarps / 2);
+      mbar_init(&bar_afree[a], GE::kIss);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar_dfull[b], GE::kIss);
+      mbar_init(&bar_dempty[b], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(&s_tmem, 512);
+  for (int i = tid; i < p.n_ratio * K; i += blockDim.x) s_rpow[i] = p.ratio_pow[i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+
+  if (warp == kProducerWarp) {
+    // ------------------------------------------------------------ producer: unit records + token tiles
+    if (lane == 0) {
+      PH_DECL
+      // weights are immutable: the first records start before the previous kernel (the relayout) has finished
+      const int pre = S < n ? S : n;
+      for (int k = 0; k < pre; ++k) {
+        mbar_expect_tx(&bar_full[k], unit_bytes(V0 + k) + GE::kBBytes);
+        bulk_g2s(smem + k * kStage, unit_src(V0 + k), unit_bytes(V0 + k), &bar_full[k]);
+      }
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      for (int k = 0; k < pre; ++k)
+        bulk_g2s(smem + k * kStage + kUnitSlot, p.xc + (size_t)((V0 + k) % NG) * GE::kBBytes, GE::kBBytes,
+                 &bar_full[k]);
+      int s = 0, eph = 0;                                     // stage of unit k and the parity of its last use
+      for (int k = pre; k < n; ++k) {
+        PH(2);
+        mbar_wait_sleep(&bar_empty[s], eph);
+        PH(0);
+        mbar_expect_tx(&bar_full[s], unit_bytes(V0 + k) + GE::kBBytes);
+        bulk_g2s(smem + s * kStage, unit_src(V0 + k), unit_bytes(V0 + k), &bar_full[s]);
+        bulk_g2s(smem + s * kStage + kUnitSlot, p.xc + (size_t)((V0 + k) % NG) * GE::kBBytes, GE::kBBytes,
+                 &bar_full[s]);
+        PH(1);
+        if (++s == S) { s = 0; eph ^= 1; }
+      }
+      PH_DUMP(24);
+    }
+  } else if (warp >= kIssuerWarp) {
+    // ------------------------------------------------------------ MMA issuer i: K-slices q = i kQ .. i kQ + kQ - 1
+    const int iss = warp - kIssuerWarp;
+    if (lane == 0 && iss < GE::kIss) {
+      PH_DECL
+      int g = V0 % NG, seg = 0, s = 0, sph = 0;
+      for (int k = 0; k < n; ++k) {
+        const int a = k & (kAS - 1);
+        const bool first = k == 0 || g == 0, last = k == n - 1 || g == NG - 1;
+        const int db = seg % GE::kDB;
+        if (first && seg >= GE::kDB) mbar_wait_sleep(&bar_dempty[db], ((seg / GE::kDB) - 1) & 1);
+        PH(0);
+        mbar_wait_sleep(&bar_full[s], sph);
+        mbar_wait_sleep(&bar_afull[a], (k >> 2) & 1);
+        tc_fence_after();
+        PH(1);
+        const uint32_t tA = tmem + GE::kACol + 64 * a;
+        const uint32_t tD = tmem + NT * (db * GE::kIss + iss);
+        const uint32_t bbase = smem_u32(smem + s * kStage + kUnitSlot);
+#pragma unroll
+        for (int qi = 0; qi < GE::kQ; ++qi) {
+          const int q = iss * GE::kQ + qi;
+          mma_f16_ts(tD, tA + 8 * q, smem_desc(bbase + q * NT * 32, 128, 256), GE::kIdesc, (first && qi == 0) ? 0u : 1u);
+        }
+        mma_commit(&bar_afree[a]);
+        mma_commit(&bar_empty[s]);
+        if (last) {
+          mma_commit(&bar_dfull[db]);
+          ++seg;
+        }
+        PH(2);
+        g = g + 1 == NG ? 0 : g + 1;
+        if (++s == S) { s = 0; sph ^= 1; }
+      }
+      if (iss == 0) PH_DUMP(16);
+    }
+  } else if (warp < kDeqWarps) {
+    // ------------------------------------------------------------ FP16 decompression (thread = row = TMEM lane)
+    // two groups of 8 warps take alternate units (one group's waits overlap the other's arithmetic); in a group,
+    // warp (lane quarter lq, half h) decompresses the 64 elements of words 2h, 2h + 1 of its 32 rows
+    const int grp = warp >> 3, lq = warp & 3, h = (warp >> 2) & 1;
+    const int r = 32 * lq + lane;
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    const int swz = chunk_swizzle(K, r);
+    int rb = V0 / NG, g = V0 % NG;
+    int s = 0, sph = 0;                                       // stage and its phase parity for unit k
+    for (int i = 0; i < grp && i < n; ++i) {
+      g = g + 1 == NG ? 0 : g + 1;
+      if (g == 0) ++rb;
+      if (++s == S) { s = 0; sph ^= 1; }
+    }
+    PH_DECL
+    for (int k = grp; k < n; k += 2) {
+      const int a = k & (kAS - 1);
+      const int rows = rows_of(rb);
+      PH(5);
+      mbar_wait_sleep(&bar_full[s], sph);
+      PH(0);
+      const uint8_t* sl = smem + s * kStage;
+      uint2 w2[K];
+      uint32_t sbw = 0u;
+      int ri = 0;
+      if (r < rows) {
+#pragma unroll
+        for (int t = 0; t < K; ++t) w2[t] = *reinterpret_cast<const uint2*>(sl + r * 16 * K + 16 * (t ^ swz) + 8 * h);
+        sbw = *reinterpret_cast<const uint32_t*>(sl + rows * 16 * K + 4 * r);
+        ri = sl[rows * (16 * K + 4) + r];
+      } else {
+#pragma unroll
+        for (int t = 0; t < K; ++t) w2[t] = make_uint2(0u, 0u);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_empty[s]);            // this warp is done with the record
+      // c16_t = fp16(fmaf(s, r^t, b)) (reading A25)
+      const float s_ = __half2float(__ushort_as_half((unsigned short)(sbw & 0xffffu)));
+      const float b_ = __half2float(__ushort_as_half((unsigned short)(sbw >> 16)));
+      PH(1);
+      __half c16[K];
+      bool fast = true;
+#pragma unroll
+      for (int t = 0; t < K; ++t) {
+        c16[t] = __float2half_rn(fmaf(s_, s_rpow[ri * K + t], b_));
+        fast = fast && __hlt(__habs(c16[t]), __float2half(32.0f));
+      }
+      uint32_t out[32];
+      if (fast) {
+        __half2 k12[K], k13[K];
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+          k12[t] = __half2half2(__hmul(c16[t], __float2half(2048.0f)));   // exact: power-of-two scaling, no overflow
+          k13[t] = __half2half2(__hmul(c16[t], __float2half(128.0f)));
+        }
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int jp = 0; jp < 8; ++jp) {
+            const int j = 2 * jp;
+            __half2 acc0 = __float2half2_rn(0.f), acc1 = __float2half2_rn(0.f);
+#pragma unroll
+            for (int t = 0; t < K; ++t) {
+              const uint32_t wt = cc ? w2[t].y : w2[t].x;
+              const uint32_t x = rot_fma(wt, 12 - j);
+              acc0 = __hfma2(bits_h2(x & 0x10001000u), k12[t], acc0);
+              acc1 = __hfma2(bits_h2(x & 0x20002000u), k13[t], acc1);
+            }
+            out[16 * cc + j] = h2_bits(acc0);
+            out[16 * cc + j + 1] = h2_bits(acc1);
+          }
+      } else {
+        // the same HFMA2 sequence with the bits as 0 / 1.0 (exactly beta * c16 per product)
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            __half2 acc = __float2half2_rn(0.f);
+#pragma unroll
+            for (int t = 0; t < K; ++t) {
+              const uint32_t wt = cc ? w2[t].y : w2[t].x;
+              acc = __hfma2(bits_h2(((wt >> j) & 0x00010001u) * 0x3C00u), __half2half2(c16[t]), acc);
+            }
+            out[16 * cc + j] = h2_bits(acc);
+          }
+      }
+      PH(2);
+      if (k >= kAS) mbar_wait_sleep(&bar_afree[a], ((k >> 2) - 1) & 1);   // MMAs of unit k - kAS done with slot a
+      tc_fence_after();
+      PH(3);
+      tmem_st32(tmem + lane_base + GE::kACol + 64 * a + 32 * h, out);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_afull[a]);
+      PH(4);
+      for (int i = 0; i < 2; ++i) {
+        g = g + 1 == NG ? 0 : g + 1;
+        if (g == 0) ++rb;
+        if (++s == S) { s = 0; sph ^= 1; }
+      }
+    }
+    if (warp == 0) PH_DUMP(0);
+  } else {
+    // ------------------------------------------------------------ epilogue (thread = row = TMEM lane)
+    asm volatile("griddepcontrol.wait;" ::: "memory");      // Y and the workspace from here on
+    const int lq = warp & 3;
+    const int r = 32 * lq + lane;
+    const int etid = (warp - kDeqWarps) * 32 + lane;         // 0 .. 127
+    const uint32_t lane_base = (uint32_t)(32 * lq) << 16;
+    constexpr int CH = NT < 32 ? NT : 32;
+    int seg = 0;
+    PH_DECL
+    for (int u = V0; u < V1;) {
+      const int rb = u / NG;
+      const int u_end = min(V1, (rb + 1) * NG);
+      const int rows = rows_of(rb);
+      const int db = seg % GE::kDB;
+      const bool shared = (long)rb * NG < V0 || (long)(rb + 1) * NG > V1;
+      const int myslot = rb == V0 / NG ? 0 : 1;
+      float* part = p.ws_part + ((size_t)cta * 2 + myslot) * (NT * 128);
+      PH(3);
+      mbar_wait_sleep(&bar_dfull[db], (seg / GE::kDB) & 1);
+      tc_fence_after();
+      PH(0);
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT; c0 += CH) {
+        uint32_t v[CH];
+        tmem_ld<CH>(tmem + lane_base + NT * (db * GE::kIss) + c0, v);
+        tmem_wait_ld();
+        pin<CH>(v);
+#pragma unroll
+        for (int i2 = 1; i2 < GE::kIss; ++i2) {                // D_0 + D_1 + ... in issuer order
+          uint32_t v2[CH];
+          tmem_ld<CH>(tmem + lane_base + NT * (db * GE::kIss + i2) + c0, v2);
+          tmem_wait_ld();
+          pin<CH>(v2);
+#pragma unroll
+          for (int i = 0; i < CH; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(v2[i]));
+        }
+        if (!shared) {
+          if (r < rows)
+#pragma unroll
+            for (int i = 0; i < CH; ++i)
+              if (c0 + i < p.ntok) p.Y[(size_t)(c0 + i) * p.M + (size_t)rb * 128 + r] = __uint_as_float(v[i]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < CH; ++i) __stcg(part + (c0 + i) * 128 + r, __uint_as_float(v[i]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_dempty[db]);
+      PH(1);
+      if (shared) {
+        named_bar(1, kEpiWarps * 32);
+        if (etid == 0) s_old = atomicAdd(p.ws_cnt + rb, 1u);
+        named_bar(1, kEpiWarps * 32);
+        const int cc0 = unit_cta(rb * NG, p.qq, p.rr), cc1 = unit_cta((rb + 1) * NG - 1, p.qq, p.rr);
+        // at rest the counter is 0xFFFFFFFF: the k-th arrival reads k - 2 (mod 2^32)
+        if (s_old + 2u == (unsigned int)(cc1 - cc0 + 1)) {
+#pragma unroll 1
+          for (int c0 = 0; c0 < NT; c0 += CH) {
+            float sum[CH];
+#pragma unroll
+            for (int i = 0; i < CH; ++i) sum[i] = 0.f;
+            for (int cc = cc0; cc <= cc1; ++cc) {         // contributors in CTA order: deterministic
+              const int sl2 = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
+              const float* src = p.ws_part + ((size_t)cc * 2 + sl2) * (NT * 128) + (size_t)c0 * 128 + r;
+              uint32_t wv[CH];
+              for (long spins = 0;; ++spins) {           // one batch per contributor, reloaded while any is unset
+                bool miss = false;
+#pragma unroll
+                for (int i = 0; i < CH; ++i) {
+                  wv[i] = ld_relaxed_u32(src + i * 128);
+                  miss |= wv[i] == kSentinel;
+                }
+                if (!miss) break;
+                if (spins > (1L << 26)) __trap();        // stores already issued never landed: fail loudly
+              }
+#pragma unroll
+              for (int i = 0; i < CH; ++i) sum[i] += __uint_as_float(wv[i]);
+            }
+            if (r < rows)
+#pragma unroll
+              for (int i = 0; i < CH; ++i)
+                if (c0 + i < p.ntok) p.Y[(size_t)(c0 + i) * p.M + (size_t)rb * 128 + r] = sum[i];
+          }
+          for (int cc = cc0; cc <= cc1; ++cc) {
+            const int sl2 = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
+            unsigned int* dst = reinterpret_cast<unsigned int*>(p.ws_part) + ((size_t)cc * 2 + sl2) * (NT * 128);
+            for (int i = 0; i < NT; ++i) dst[i * 128 + r] = kSentinel;
+          }
+          if (etid == 0) p.ws_cnt[rb] = kSentinel;
+        }
+      }
+      PH(2);
+      ++seg;
+      u = u_end;
+    }
+    if (warp == kDeqWarps) PH_DUMP(8);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static int num_sms() {
+  static int nsm[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!nsm[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    nsm[dev] = v > 0 ? v : 148;
+  }
+  return nsm[dev];
+}
+
+struct Plan {
+  int NG, n_full, tail_rows, n_rb, Us, C, NT, passes;
+};
+static int nt_for(int ntok) {
+  return ntok <= 16 ? 16 : ntok <= 32 ? 32 : ntok <= 64 ? 64 : ntok <= 128 ? 128 : 256;
+}
+static Plan make_plan(const sbvr_weights* w, int T) {
+  Plan pl;
+  pl.NG = w->N / kG;
+  pl.n_full = w->M / kRowBlock;
+  pl.tail_rows = w->M % kRowBlock;
+  pl.n_rb = pl.n_full + (pl.tail_rows ? 1 : 0);
+  pl.Us = pl.n_rb * pl.NG;
+  const int by_units = (pl.Us + PF_MIN_UNITS - 1) / PF_MIN_UNITS;
+  pl.C = num_sms() < by_units ? num_sms() : (by_units < 1 ? 1 : by_units);
+  pl.NT = nt_for(T < kMaxNT ? T : kMaxNT);
+  pl.passes = (T + kMaxNT - 1) / kMaxNT;
+  return pl;
+}
+static size_t cnt_bytes(const Plan& pl) { return ((size_t)(pl.n_rb + 1) * 4 + 255) / 256 * 256; }
+static size_t part_bytes(const Plan& pl) { return (size_t)pl.C * 2 * pl.NT * 128 * sizeof(float); }
+static size_t xc_bytes(const Plan& pl) { return (size_t)pl.passes * pl.NG * pl.NT * 128 * 2; }
+
+template <int K, int NT>
+static int stages() {
+  const int stage = (128 * (16 * K + 5) + 127) / 128 * 128 + Geo<NT>::kBBytes;
+  int s = kSmemBudget / stage;
+  return s > 6 ? 6 : s;
+}
+
+template <int K, int NT>
+static cudaError_t launch_one(const PfParams& p, int C, cudaStream_t st) {
+  const int S = stages<K, NT>();
+  const int smem = S * ((128 * (16 * K + 5) + 127) / 128 * 128 + Geo<NT>::kBBytes);
+  static bool attr[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_kernel<K, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) attr[dev] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, prefill_kernel<K, NT>, p, S);
+}
+
+template <int K>
+static cudaError_t launch_k(const PfParams& p, int C, int NT, cudaStream_t st) {
+  switch (NT) {
+    case 16: return launch_one<K, 16>(p, C, st);
+    case 32: return launch_one<K, 32>(p, C, st);
+    case 64: return launch_one<K, 64>(p, C, st);
+    case 128: return launch_one<K, 128>(p, C, st);
+    default: return launch_one<K, 256>(p, C, st);
+  }
+}
+
+}  // namespace pf
+
+size_t prefill_workspace_bytes(const sbvr_weights* w, int T) {
+  const pf::Plan pl = pf::make_plan(w, T);
+  return pf::cnt_bytes(pl) + pf::part_bytes(pl) + pf::xc_bytes(pl);
+}
+
+sbvr_status launch_prefill(const sbvr_weights* w, const uint16_t* X, int T, float* Y, void* ws, size_t ws_bytes,
+                           cudaStream_t st) {
+  using namespace pf;
+  if (w->K < 1 || w->K > kMaxPlanes) return set_error(SBVR_ERR_UNSUPPORTED, "prefill: K <= 4 only (K=%d)", w->K);
+  const Plan pl = make_plan(w, T);
+  if (!ws || ws_bytes < prefill_workspace_bytes(w, T))
+    return set_error(SBVR_ERR_WORKSPACE, "prefill: workspace %zu bytes < required %zu", ws_bytes,
+                     prefill_workspace_bytes(w, T));
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint8_t* xc = base + cnt_bytes(pl) + part_bytes(pl);
+  {
+    const long rows16 = (long)pl.passes * pl.NG * pl.NT * 16;
+    const long blocks = (rows16 + 255) / 256;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(blocks < 4 * 148 ? blocks : 4 * 148));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, pf_relayout_kernel, X, T, w->N, pl.NT, pl.passes, xc);
+    if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "prefill relayout: %s", cudaGetErrorString(e));
+    sbvr_status s = check_launch("pf_relayout_kernel");
+    if (s != SBVR_OK) return s;
+  }
+  PfParams p;
+  p.units = w->data;
+  p.ratio_pow = w->ratio_pow;
+  p.M = w->M;
+  p.N = w->N;
+  p.n_ratio = w->n_ratio;
+  p.n_full = pl.n_full;
+  p.tail_rows = pl.tail_rows;
+  p.Us = pl.Us;
+  p.qq = pl.Us / pl.C;
+  p.rr = pl.Us % pl.C;
+  p.ws_cnt = reinterpret_cast<unsigned int*>(base);
+  p.ws_part = reinterpret_cast<float*>(base + cnt_bytes(pl));
+  {
+    const char* tsp = getenv("SBVR_TS_PTR");
+    p.ts = tsp ? reinterpret_cast<unsigned long long*>(strtoull(tsp, nullptr, 0)) : nullptr;
+  }
+  for (int pass = 0; pass < pl.passes; ++pass) {
+    const int done = pass * kMaxNT;
+    p.ntok = T - done < kMaxNT ? T - done : kMaxNT;
+    p.xc = xc + (size_t)pass * pl.NG * pl.NT * 128 * 2;
+    p.Y = Y + (size_t)done * w->M;
+    cudaError_t e;
+    switch (w->K) {
+      case 1: e = launch_k<1>(p, pl.C, pl.NT, st); break;
+      case 2: e = launch_k<2>(p, pl.C, pl.NT, st); break;
+      case 3: e = launch_k<3>(p, pl.C, pl.NT, st); break;
+      default: e = launch_k<4>(p, pl.C, pl.NT, st); break;
+    }
+    if (e != cudaSuccess) return set_error(SBVR_ERR_CUDA, "prefill setup: %s", cudaGetErrorString(e));
+    sbvr_status s = check_launch("prefill_kernel");
+    if (s != SBVR_OK) return s;
+  }
+  return SBVR_OK;
+}
+
+}  // namespace sbvr

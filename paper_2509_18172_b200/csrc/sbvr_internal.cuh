@@ -133,6 +133,9 @@ struct GroupPeers {       // fused all-gather of a grouped GEMV: y[i * n + j] = 
 sbvr_status launch_gemv_group(const sbvr_gemv_problem* pr, int n, void* ws, size_t ws_bytes, cudaStream_t st,
                               const GroupPeers* peers = nullptr);
 size_t group_workspace_bytes(const sbvr_gemv_problem* pr, int n);
+sbvr_status launch_prefill(const sbvr_weights* w, const uint16_t* X, int T, float* Y, void* ws, size_t ws_bytes,
+                           cudaStream_t st);
+size_t prefill_workspace_bytes(const sbvr_weights* w, int T);
 sbvr_status launch_hadamard(const void* X, void* Y, int dtype, int rows, int N, int b, const int8_t* signs,
                             cudaStream_t st);
 
