@@ -17,7 +17,7 @@
 // element pairs (j, j + 16) of each 32-element word; the pre-pass lays the tokens out in the same K order.
 //
 // CTA = one SM, persistent over a balanced contiguous range of (128-row block, group) units (the records of
-// include/sbvr.h), 25 warps:
+// include/sbvr.h), 26 warps:
 //   warps 0..15   decompression, thread = row = TMEM lane; two groups of 8 warps take alternate units; warp w:
 //                 lane quarter w % 4, words 2h, 2h + 1 (h = (w / 4) % 2): K plane words -> 32 half2 columns ->
 //                 tcgen05.st into a 4-slot A ring in tensor memory
@@ -26,7 +26,8 @@
 //   warps 20..23  MMA issuers: 8 x tcgen05.mma kind::f16 (M = 128, N = NT, K = 16) per unit, A from TMEM,
 //                 B (the tokens' group slice, canonical K-major layout) from shared memory; up to 4 issuers
 //                 split the 8 K-slices, each into its own accumulator, summed in order by the epilogue
-//   warp 24       producer: cp.async.bulk of the unit record and of the tokens' group slice into an S-stage ring
+//   warp 24       producer of the unit records: cp.async.bulk into a deep ring released by the decompression warps
+//   warp 25       producer of the token tiles: cp.async.bulk of the tokens' group slice into a ring released by the MMAs
 #include <cstdlib>
 
 #include "ptx_sm100.cuh"
@@ -40,13 +41,25 @@ using namespace ptx;
 constexpr int kDeqWarps = 16;
 constexpr int kEpiWarps = 4;
 constexpr int kIssuerWarp = kDeqWarps + kEpiWarps;   // first of 4 issuer warps (one per SM sub-partition)
-constexpr int kProducerWarp = kIssuerWarp + 4;
-constexpr int kThreads = (kProducerWarp + 1) * 32;
+constexpr int kProducerWarp = kIssuerWarp + 4;     // + 0: weight records, + 1: token tiles
+constexpr int kThreads = (kProducerWarp + 2) * 32;
+constexpr int kMaxSW = 16, kMaxSB = 4;
 constexpr int kAS = 4;              // A slots (units in flight between decompression and MMA; a power of 2)
 constexpr int kMaxNT = 256;         // tokens per weight pass (MMA N)
 constexpr int kMaxPlanes = 4;
 constexpr int kSmemBudget = 220 * 1024;
 constexpr unsigned int kSentinel = 0xFFFFFFFFu;
+#ifndef PF_ABL
+#define PF_ABL 0   // ablation bits (diagnostic builds only): 1 no decompression arithmetic, 2 no MMAs
+#endif
+#ifndef PF_SPIN
+#define PF_SPIN 0   // 1: the critical-path waits (records, A slots, token tiles) spin instead of suspending
+#endif
+#if PF_SPIN
+#define PF_WAIT_CRIT(bar, ph) mbar_wait(bar, ph)
+#else
+#define PF_WAIT_CRIT(bar, ph) mbar_wait_sleep(bar, ph)
+#endif
 #ifndef PF_MIN_UNITS
 #define PF_MIN_UNITS 8
 #endif
@@ -140,21 +153,29 @@ __device__ __forceinline__ uint32_t rot_fma(uint32_t w, int sh) {
   else asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(w), "r"(1u << (32 + sh)));
   return r;
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 bits_h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 
 // ------------------------------------------------------------------ main kernel
 template <int K, int NT>
-__global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S) {
+__global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW, int SB) {
   static_assert(K >= 1 && K <= kMaxPlanes, "K");
   using GE = Geo<NT>;
   constexpr int kUnitFull = 128 * (16 * K + 5);
   constexpr int kUnitSlot = (kUnitFull + 127) / 128 * 128;
-  constexpr int kStage = kUnitSlot + GE::kBBytes;
   extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* const sW = smem;                                // SW unit records
+  uint8_t* const sBt = smem + SW * kUnitSlot;              // SB token tiles
   __shared__ float s_rpow[64 * kMaxPlanes];
-  __shared__ __align__(8) uint64_t bar_full[8];
-  __shared__ __align__(8) uint64_t bar_empty[8];
+  __shared__ __align__(8) uint64_t bar_wfull[kMaxSW];
+  __shared__ __align__(8) uint64_t bar_wempty[kMaxSW];
+  __shared__ __align__(8) uint64_t bar_bfull[kMaxSB];
+  __shared__ __align__(8) uint64_t bar_bempty[kMaxSB];
   __shared__ __align__(8) uint64_t bar_afull[kAS];
   __shared__ __align__(8) uint64_t bar_afree[kAS];
   __shared__ __align__(8) uint64_t bar_dfull[2];
@@ -179,9 +200,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S)
   auto rows_of = [&](int rb) { return rb < p.n_full ? 128 : p.tail_rows; };
 
   if (tid == kProducerWarp * 32) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&bar_full[s], 1);
-      mbar_init(&bar_empty[s], kDeqWarps / 2 + GE::kIss);
+    for (int s = 0; s < SW; ++s) {
+      mbar_init(&bar_wfull[s], 1);
+      mbar_init(&bar_wempty[s], kDeqWarps / 2);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&bar_bfull[s], 1);
+      mbar_init(&bar_bempty[s], GE::kIss);
     }
     for (int a = 0; a < kAS; ++a) {
       mbar_init(&bar_afull[a], kDeqWarps / 2);
@@ -201,37 +226,42 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S)
   const uint32_t tmem = s_tmem;
 
   if (warp == kProducerWarp) {
-    // ------------------------------------------------------------ producer: unit records + token tiles
+    // ------------------------------------------------------------ producer of the unit records (SW-deep ring, released
+    // by the decompression warps as soon as they have read a record: the weight stream runs far ahead of the MMAs)
     if (lane == 0) {
       PH_DECL
-      // weights are immutable: the first records start before the previous kernel (the relayout) has finished
-      const int pre = S < n ? S : n;
-      for (int k = 0; k < pre; ++k) {
-        mbar_expect_tx(&bar_full[k], unit_bytes(V0 + k) + GE::kBBytes);
-        bulk_g2s(smem + k * kStage, unit_src(V0 + k), unit_bytes(V0 + k), &bar_full[k]);
-      }
-      asm volatile("griddepcontrol.wait;" ::: "memory");
-      for (int k = 0; k < pre; ++k)
-        bulk_g2s(smem + k * kStage + kUnitSlot, p.xc + (size_t)((V0 + k) % NG) * GE::kBBytes, GE::kBBytes,
-                 &bar_full[k]);
-      int s = 0, eph = 0;                                     // stage of unit k and the parity of its last use
-      for (int k = pre; k < n; ++k) {
+      int s = 0, use = 0;                                     // stage of unit k and the parity of its use count
+      for (int k = 0; k < n; ++k) {
         PH(2);
-        mbar_wait_sleep(&bar_empty[s], eph);
+        if (k >= SW) mbar_wait_sleep(&bar_wempty[s], use ^ 1);   // release of the previous use (weights are immutable:
+                                                                  // no griddepcontrol.wait)
         PH(0);
-        mbar_expect_tx(&bar_full[s], unit_bytes(V0 + k) + GE::kBBytes);
-        bulk_g2s(smem + s * kStage, unit_src(V0 + k), unit_bytes(V0 + k), &bar_full[s]);
-        bulk_g2s(smem + s * kStage + kUnitSlot, p.xc + (size_t)((V0 + k) % NG) * GE::kBBytes, GE::kBBytes,
-                 &bar_full[s]);
+        mbar_expect_tx(&bar_wfull[s], unit_bytes(V0 + k));
+        bulk_g2s(sW + s * kUnitSlot, unit_src(V0 + k), unit_bytes(V0 + k), &bar_wfull[s]);
         PH(1);
-        if (++s == S) { s = 0; eph ^= 1; }
+        if (++s == SW) { s = 0; use ^= 1; }
       }
       PH_DUMP(24);
     }
+  } else if (warp == kProducerWarp + 1) {
+    // ------------------------------------------------------------ producer of the token tiles (SB-deep ring, released
+    // by the MMA commits); the tiles are the relayout kernel's output
+    if (lane == 0) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      int s = 0, use = 0;
+      for (int k = 0; k < n; ++k) {
+        if (k >= SB) mbar_wait_sleep(&bar_bempty[s], use ^ 1);
+        mbar_expect_tx(&bar_bfull[s], GE::kBBytes);
+        bulk_g2s(sBt + s * GE::kBBytes, p.xc + (size_t)((V0 + k) % NG) * GE::kBBytes, GE::kBBytes, &bar_bfull[s]);
+        if (++s == SB) { s = 0; use ^= 1; }
+      }
+    }
   } else if (warp >= kIssuerWarp) {
     // ------------------------------------------------------------ MMA issuer i: K-slices q = i kQ .. i kQ + kQ - 1
+    // (the whole warp runs the loop -- warp-uniform control flow, no per-lane issue loop around each tcgen05
+    // instruction -- and one elected lane issues)
     const int iss = warp - kIssuerWarp;
-    if (lane == 0 && iss < GE::kIss) {
+    if (iss < GE::kIss) {
       PH_DECL
       int g = V0 % NG, seg = 0, s = 0, sph = 0;
       for (int k = 0; k < n; ++k) {
@@ -240,27 +270,29 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S)
         const int db = seg % GE::kDB;
         if (first && seg >= GE::kDB) mbar_wait_sleep(&bar_dempty[db], ((seg / GE::kDB) - 1) & 1);
         PH(0);
-        mbar_wait_sleep(&bar_full[s], sph);
-        mbar_wait_sleep(&bar_afull[a], (k >> 2) & 1);
+        PF_WAIT_CRIT(&bar_bfull[s], sph);
+        PF_WAIT_CRIT(&bar_afull[a], (k >> 2) & 1);
         tc_fence_after();
         PH(1);
         const uint32_t tA = tmem + GE::kACol + 64 * a;
         const uint32_t tD = tmem + NT * (db * GE::kIss + iss);
-        const uint32_t bbase = smem_u32(smem + s * kStage + kUnitSlot);
+        const uint32_t bbase = smem_u32(sBt + s * GE::kBBytes);
+        if (elect_one()) {
 #pragma unroll
-        for (int qi = 0; qi < GE::kQ; ++qi) {
-          const int q = iss * GE::kQ + qi;
-          mma_f16_ts(tD, tA + 8 * q, smem_desc(bbase + q * NT * 32, 128, 256), GE::kIdesc, (first && qi == 0) ? 0u : 1u);
+          for (int qi = 0; qi < GE::kQ; ++qi) {
+            const int q = iss * GE::kQ + qi;
+            if (!(PF_ABL & 2))
+              mma_f16_ts(tD, tA + 8 * q, smem_desc(bbase + q * NT * 32, 128, 256), GE::kIdesc, (first && qi == 0) ? 0u : 1u);
+          }
+          mma_commit(&bar_afree[a]);
+          mma_commit(&bar_bempty[s]);
+          if (last) mma_commit(&bar_dfull[db]);
         }
-        mma_commit(&bar_afree[a]);
-        mma_commit(&bar_empty[s]);
-        if (last) {
-          mma_commit(&bar_dfull[db]);
-          ++seg;
-        }
+        __syncwarp();
+        if (last) ++seg;
         PH(2);
         g = g + 1 == NG ? 0 : g + 1;
-        if (++s == S) { s = 0; sph ^= 1; }
+        if (++s == SB) { s = 0; sph ^= 1; }
       }
       if (iss == 0) PH_DUMP(16);
     }
@@ -277,16 +309,16 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S)
     for (int i = 0; i < grp && i < n; ++i) {
       g = g + 1 == NG ? 0 : g + 1;
       if (g == 0) ++rb;
-      if (++s == S) { s = 0; sph ^= 1; }
+      if (++s == SW) { s = 0; sph ^= 1; }
     }
     PH_DECL
     for (int k = grp; k < n; k += 2) {
       const int a = k & (kAS - 1);
       const int rows = rows_of(rb);
       PH(5);
-      mbar_wait_sleep(&bar_full[s], sph);
+      PF_WAIT_CRIT(&bar_wfull[s], sph);
       PH(0);
-      const uint8_t* sl = smem + s * kStage;
+      const uint8_t* sl = sW + s * kUnitSlot;
       uint2 w2[K];
       uint32_t sbw = 0u;
       int ri = 0;
@@ -300,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S)
         for (int t = 0; t < K; ++t) w2[t] = make_uint2(0u, 0u);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_empty[s]);            // this warp is done with the record
+      if (lane == 0) mbar_arrive(&bar_wempty[s]);           // this warp is done with the record
       // c16_t = fp16(fmaf(s, r^t, b)) (reading A25)
       const float s_ = __half2float(__ushort_as_half((unsigned short)(sbw & 0xffffu)));
       const float b_ = __half2float(__ushort_as_half((unsigned short)(sbw >> 16)));
@@ -313,7 +345,10 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S)
         fast = fast && __hlt(__habs(c16[t]), __float2half(32.0f));
       }
       uint32_t out[32];
-      if (fast) {
+      if (PF_ABL & 1) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) out[i] = w2[i & (K - 1)].x ^ (uint32_t)i;
+      } else if (fast) {
         __half2 k12[K], k13[K];
 #pragma unroll
         for (int t = 0; t < K; ++t) {
@@ -352,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S)
           }
       }
       PH(2);
-      if (k >= kAS) mbar_wait_sleep(&bar_afree[a], ((k >> 2) - 1) & 1);   // MMAs of unit k - kAS done with slot a
+      if (k >= kAS) PF_WAIT_CRIT(&bar_afree[a], ((k >> 2) - 1) & 1);   // MMAs of unit k - kAS done with slot a
       tc_fence_after();
       PH(3);
       tmem_st32(tmem + lane_base + GE::kACol + 64 * a + 32 * h, out);
@@ -364,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int S)
       for (int i = 0; i < 2; ++i) {
         g = g + 1 == NG ? 0 : g + 1;
         if (g == 0) ++rb;
-        if (++s == S) { s = 0; sph ^= 1; }
+        if (++s == SW) { s = 0; sph ^= 1; }
       }
     }
     if (warp == 0) PH_DUMP(0);
@@ -514,16 +549,18 @@ static size_t part_bytes(const Plan& pl) { return (size_t)pl.C * 2 * pl.NT * 128
 static size_t xc_bytes(const Plan& pl) { return (size_t)pl.passes * pl.NG * pl.NT * 128 * 2; }
 
 template <int K, int NT>
-static int stages() {
-  const int stage = (128 * (16 * K + 5) + 127) / 128 * 128 + Geo<NT>::kBBytes;
-  int s = kSmemBudget / stage;
-  return s > 6 ? 6 : s;
+static void stages(int& SW, int& SB) {
+  const int unit = (128 * (16 * K + 5) + 127) / 128 * 128;
+  SB = NT <= 32 ? 4 : NT <= 128 ? 3 : 2;
+  SW = (kSmemBudget - SB * Geo<NT>::kBBytes) / unit;
+  if (SW > kMaxSW) SW = kMaxSW;
 }
 
 template <int K, int NT>
 static cudaError_t launch_one(const PfParams& p, int C, cudaStream_t st) {
-  const int S = stages<K, NT>();
-  const int smem = S * ((128 * (16 * K + 5) + 127) / 128 * 128 + Geo<NT>::kBBytes);
+  int SW, SB;
+  stages<K, NT>(SW, SB);
+  const int smem = SW * ((128 * (16 * K + 5) + 127) / 128 * 128) + SB * Geo<NT>::kBBytes;
   static bool attr[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -542,7 +579,7 @@ static cudaError_t launch_one(const PfParams& p, int C, cudaStream_t st) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, prefill_kernel<K, NT>, p, S);
+  return cudaLaunchKernelEx(&cfg, prefill_kernel<K, NT>, p, SW, SB);
 }
 
 template <int K>
