@@ -690,6 +690,41 @@ def _group_record(sb, device, config, mats, P=1, iters=30, seed=0):
             "pct_measured_peak": round(100 * gbps / peak, 2), "ring": ring}
 
 
+def _tensor_peak():
+    """Measured dense bf16 TF/s (MEASURED_PEAKS.json, burst); fp16 runs at the bf16 rate (guide's nominal ratio 1)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, burst; fp16 = bf16 rate)"
+    except Exception:
+        return 2250.0, "fallback (nominal 2.25 PFLOP/s dense fp16)"
+
+
+def _prefill_record(sb, device, config, name, M, N, T, iters=20, seed=0):
+    """f1 prefill (sbvr_prefill): us per call median/p10/p90 over graph replays on a ring of distinct weight
+    copies (> L2), the weight stream's algorithmic GB/s (compressed bytes), the GEMM's TFLOP/s against the measured
+    dense fp16 peak, cuBLAS fp16 GEMM at the same (M, N, T) and the speedup."""
+    pc, s16, b16, ri = synthetic.random_encoded(M, N, K_BITS, N_RATIO, seed=seed + M + N)
+    w0 = sb.pack_canonical(pc, s16, b16, ri, N_RATIO, device=device)
+    ring = _ring_count(w0.nbytes)
+    ws_ = [w0] + [sb.SbvrWeights(M, N, K_BITS, N_RATIO, w0.data.clone(), w0.ratio_pow.clone()) for _ in range(ring - 1)]
+    wsp = [sb.prefill_workspace(w, T) for w in ws_]
+    X = torch.from_numpy(synthetic.activation(N, seed=7, T=T)).to(device)
+    Y = torch.empty(T, M, dtype=torch.float32, device=device)
+    stream = torch.cuda.Stream(device)
+    med, p10, p90 = _graph_stats(stream, lambda i: sb.prefill(ws_[i % ring], X, Y, wsp[i % ring]), iters)
+    wbytes = M * N * K_BITS // 8 + 5 * M * N // 128
+    tflops = 2.0 * M * N * T / (med * 1e-6) / 1e12
+    tpeak, _ = _tensor_peak()
+    del ws_, wsp
+    torch.cuda.empty_cache()
+    cu = _cublas_us(device, M, N, T)
+    return {"config": config, "shape": name, "M": M, "N": N, "K": K_BITS, "path": "prefill/fp16-decompress+tcgen05",
+            "T": T, "us_median": round(med, 3), "us_p10": round(p10, 3), "us_p90": round(p90, 3),
+            "weight_GBps": round(wbytes / (med * 1e-6) / 1e9, 1), "TFLOPs": round(tflops, 1),
+            "frac_tensor_peak": round(tflops / tpeak, 4), "ring": ring, "cublas_us": round(cu, 3),
+            "speedup_vs_cublas": round(cu / med, 3)}
+
+
 def records(device):
     """one record per (config, shape, K, path, T, P) -- C2 Llama-3-8B decode set, C3 Llama-3-70B
     MLP row shards, C4 Qwen2.5-7B K sweep on both activation paths, C5 batched T = 1..64 -- plus f3."""
@@ -713,6 +748,10 @@ def records(device):
             for kind in ("sbvr", "fp16"):
                 out.append(_record(sb, device, "C4 qwen25_7b", name, M, N, K, 1, kind, sb.ALGO_AUTO,
                                    cublas=(K == 4 and kind == "sbvr")))
+    # C6 f1 prefill (FP16 decompression + tcgen05 GEMM) on the Llama-3-8B shapes
+    for name, M, N in (("q_proj", 4096, 4096), ("gate_proj", 14336, 4096), ("down_proj", 4096, 14336)):
+        for T in (16, 64, 256):
+            out.append(_prefill_record(sb, device, "C6 llama3_8b_prefill", name, M, N, T))
     for name, M, N in (("q_proj", 4096, 4096), ("gate_proj", 14336, 4096)):
         for T in (1, 2, 4, 8, 16, 32, 64):
             out.append(_record(sb, device, "C5 llama3_8b_batched", name, M, N, K_BITS, T, "sbvr", sb.ALGO_AUTO,
