@@ -300,7 +300,7 @@ sbvr_status sbvr_hadamard_rows(const void* X, void* Y, int32_t dtype, int32_t ro
  * w16 = fl16(... fl16(beta_0 c16_0) + ... + beta_{K-1} c16_{K-1}) in plane order -- bit-identical to the
  * oracle's O-PF decode.  One pass over the weights per 256 tokens.
  *   w          SBVR_META_GROUP weights, K = 1..4, any M (multiple of 16), N multiple of 128 (device)
- *   X          device, fp16 bit patterns [T][N] row-major (2-byte aligned); read-only
+ *   X          device, fp16 bit patterns [T][N] row-major (8-byte aligned); read-only
  *   T          tokens, >= 0 (0: nothing enqueued); any size (passes of 256)
  *   Y          device, fp32 [T][M] row-major (4-byte aligned); every element written
  *   workspace  device, 256-byte aligned, >= sbvr_prefill_workspace_bytes(w, T); initialised once with

@@ -481,8 +481,8 @@ sbvr_status sbvr_prefill(const sbvr_weights* w, const uint16_t* X, int32_t T, fl
   if (s != SBVR_OK) return s;
   if (T == 0) return SBVR_OK;
   if (!X || !Y) return set_error(SBVR_ERR_INVALID_ARG, "X or Y is NULL");
-  if ((reinterpret_cast<uintptr_t>(X) & 1) || (reinterpret_cast<uintptr_t>(Y) & 3))
-    return set_error(SBVR_ERR_ALIGNMENT, "X must be 2-byte and Y 4-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(X) & 7) || (reinterpret_cast<uintptr_t>(Y) & 3))
+    return set_error(SBVR_ERR_ALIGNMENT, "X must be 8-byte and Y 4-byte aligned");
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255))
     return set_error(workspace ? SBVR_ERR_ALIGNMENT : SBVR_ERR_WORKSPACE, "workspace NULL or not 256-byte aligned");
   return launch_prefill(w, X, T, Y, workspace, ws_bytes, (cudaStream_t)stream);

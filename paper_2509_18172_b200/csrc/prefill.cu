@@ -22,7 +22,8 @@
 //                 lane quarter w % 4, words 2h, 2h + 1 (h = (w / 4) % 2): K plane words -> 32 half2 columns ->
 //                 tcgen05.st into a 4-slot A ring in tensor memory
 //   warp 16..19   epilogue, thread = row: at the end of each row-block segment tcgen05.ld of D -> Y, or the
-//                 CTA's partial to the workspace + last-arriver combine (deterministic, as gemv_zt.cu)
+//                 CTA's partial to the workspace + threadfence-reduction last-arriver combine (contributors summed
+//                 in CTA order: deterministic; the CTA's last row block is summed by all its threads at the end)
 //   warps 20..23  MMA issuers: 8 x tcgen05.mma kind::f16 (M = 128, N = NT, K = 16) per unit, A from TMEM,
 //                 B (the tokens' group slice, canonical K-major layout) from shared memory; up to 4 issuers
 //                 split the 8 K-slices, each into its own accumulator, summed in order by the epilogue
@@ -69,7 +70,7 @@ struct PfParams {
   const float* ratio_pow;   // [n_ratio][K]
   const uint8_t* xc;        // this pass: [NG][NT x 128 fp16 in the B layout below]
   float* Y;                 // this pass: [ntok][M]
-  float* ws_part;           // [CTA][2 (first / last row block)][NT][128]
+  float* ws_part;           // [CTA][2 (first / last row block)][NT][128] (any content at rest)
   unsigned int* ws_cnt;     // [row block] arrival counters (0xFFFFFFFF at rest)
   int M, N, n_ratio, ntok;
   int n_full, tail_rows;
@@ -133,12 +134,16 @@ __global__ void pf_relayout_kernel(const uint16_t* X, int T, int N, int NT, int 
     const int tok = pass * kMaxNT + 8 * ng + r;
     uint32_t v[4] = {0u, 0u, 0u, 0u};
     if (tok < T) {
+      // the row's 8 K slots are elements e0 .. e0 + 3 interleaved with e0 + 16 .. e0 + 19 (k_to_elem): two 8-byte
+      // loads and four byte permutes
       const uint16_t* row = X + (size_t)tok * N + (size_t)g * kG;
-#pragma unroll
-      for (int i2 = 0; i2 < 4; ++i2) {
-        const int kk = 16 * q + 8 * kh + 2 * i2;
-        v[i2] = (uint32_t)__ldg(row + k_to_elem(kk)) | ((uint32_t)__ldg(row + k_to_elem(kk + 1)) << 16);
-      }
+      const int e0 = k_to_elem(16 * q + 8 * kh);
+      const uint2 lo = __ldg(reinterpret_cast<const uint2*>(row + e0));
+      const uint2 hi = __ldg(reinterpret_cast<const uint2*>(row + e0 + 16));
+      v[0] = __byte_perm(lo.x, hi.x, 0x5410);
+      v[1] = __byte_perm(lo.x, hi.x, 0x7632);
+      v[2] = __byte_perm(lo.y, hi.y, 0x5410);
+      v[3] = __byte_perm(lo.y, hi.y, 0x7632);
     }
     *reinterpret_cast<uint4*>(xc + (size_t)idx * 16) = make_uint4(v[0], v[1], v[2], v[3]);
   }
@@ -182,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
   __shared__ __align__(8) uint64_t bar_dempty[2];
   __shared__ uint32_t s_tmem;
   __shared__ unsigned int s_old;
+  __shared__ int s_comb_rb;                              // >= 0: row block the whole CTA combines at the end
 
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -219,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(&s_tmem, 512);
+  if (tid == 0) s_comb_rb = -1;
   for (int i = tid; i < p.n_ratio * K; i += blockDim.x) s_rpow[i] = p.ratio_pow[i];
   tc_fence_before();
   __syncthreads();
@@ -455,12 +462,21 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
       if (lane == 0) mbar_arrive(&bar_dempty[db]);
       PH(1);
       if (shared) {
+        // threadfence reduction: every writer fences its partial before the arrival count; the last arriver fences
+        // after observing the count, then reads the others' partials (no CTA ever waits for another)
+        __threadfence();
         named_bar(1, kEpiWarps * 32);
         if (etid == 0) s_old = atomicAdd(p.ws_cnt + rb, 1u);
         named_bar(1, kEpiWarps * 32);
+        __threadfence();
         const int cc0 = unit_cta(rb * NG, p.qq, p.rr), cc1 = unit_cta((rb + 1) * NG - 1, p.qq, p.rr);
         // at rest the counter is 0xFFFFFFFF: the k-th arrival reads k - 2 (mod 2^32)
-        if (s_old + 2u == (unsigned int)(cc1 - cc0 + 1)) {
+        const bool last_arriver = s_old + 2u == (unsigned int)(cc1 - cc0 + 1);
+        if (last_arriver && u_end == V1) {
+          // the CTA's last segment: every other warp is done by now, so the whole CTA sums it after the final
+          // barrier (more loads in flight per round trip than these 4 warps can hold)
+          if (etid == 0) s_comb_rb = rb;
+        } else if (last_arriver) {
 #pragma unroll 1
           for (int c0 = 0; c0 < NT; c0 += CH) {
             float sum[CH];
@@ -469,29 +485,16 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
             for (int cc = cc0; cc <= cc1; ++cc) {         // contributors in CTA order: deterministic
               const int sl2 = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
               const float* src = p.ws_part + ((size_t)cc * 2 + sl2) * (NT * 128) + (size_t)c0 * 128 + r;
-              uint32_t wv[CH];
-              for (long spins = 0;; ++spins) {           // one batch per contributor, reloaded while any is unset
-                bool miss = false;
+              float wv[CH];
 #pragma unroll
-                for (int i = 0; i < CH; ++i) {
-                  wv[i] = ld_relaxed_u32(src + i * 128);
-                  miss |= wv[i] == kSentinel;
-                }
-                if (!miss) break;
-                if (spins > (1L << 26)) __trap();        // stores already issued never landed: fail loudly
-              }
+              for (int i = 0; i < CH; ++i) wv[i] = __ldcg(src + i * 128);
 #pragma unroll
-              for (int i = 0; i < CH; ++i) sum[i] += __uint_as_float(wv[i]);
+              for (int i = 0; i < CH; ++i) sum[i] += wv[i];
             }
             if (r < rows)
 #pragma unroll
               for (int i = 0; i < CH; ++i)
                 if (c0 + i < p.ntok) p.Y[(size_t)(c0 + i) * p.M + (size_t)rb * 128 + r] = sum[i];
-          }
-          for (int cc = cc0; cc <= cc1; ++cc) {
-            const int sl2 = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
-            unsigned int* dst = reinterpret_cast<unsigned int*>(p.ws_part) + ((size_t)cc * 2 + sl2) * (NT * 128);
-            for (int i = 0; i < NT; ++i) dst[i * 128 + r] = kSentinel;
           }
           if (etid == 0) p.ws_cnt[rb] = kSentinel;
         }
@@ -505,6 +508,39 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
 
   tc_fence_before();
   __syncthreads();
+  if (s_comb_rb >= 0) {
+    // last-arriver combine of the CTA's last row block by all threads: flat partial index f = token * 128 + row,
+    // contributors in CTA order (deterministic), one batch of loads per (block of values, contributor)
+    const int rb = s_comb_rb, rows = rows_of(rb);
+    const int cc0 = unit_cta(rb * NG, p.qq, p.rr), cc1 = unit_cta((rb + 1) * NG - 1, p.qq, p.rr);
+    constexpr int kVals = (NT * 128 + kThreads - 1) / kThreads;
+    constexpr int kB = kVals < 16 ? kVals : 16;
+#pragma unroll 1
+    for (int b0 = 0; b0 < kVals; b0 += kB) {
+      float sum[kB];
+#pragma unroll
+      for (int i = 0; i < kB; ++i) sum[i] = 0.f;
+      for (int cc = cc0; cc <= cc1; ++cc) {
+        const int sl2 = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
+        const float* src = p.ws_part + ((size_t)cc * 2 + sl2) * (NT * 128);
+        float wv[kB];
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+          const int f = tid + kThreads * (b0 + i);
+          wv[i] = f < NT * 128 ? __ldcg(src + f) : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < kB; ++i) sum[i] += wv[i];
+      }
+#pragma unroll
+      for (int i = 0; i < kB; ++i) {
+        const int f = tid + kThreads * (b0 + i);
+        const int tok = f >> 7, r = f & 127;
+        if (f < NT * 128 && tok < p.ntok && r < rows) p.Y[(size_t)tok * p.M + (size_t)rb * 128 + r] = sum[i];
+      }
+    }
+    if (tid == 0) p.ws_cnt[rb] = kSentinel;
+  }
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -551,7 +587,7 @@ static size_t xc_bytes(const Plan& pl) { return (size_t)pl.passes * pl.NG * pl.N
 template <int K, int NT>
 static void stages(int& SW, int& SB) {
   const int unit = (128 * (16 * K + 5) + 127) / 128 * 128;
-  SB = NT <= 32 ? 4 : NT <= 128 ? 3 : 2;
+  SB = NT <= 128 ? 4 : 3;          // token tiles come from L2 but are large at big NT: deep enough to hide it
   SW = (kSmemBudget - SB * Geo<NT>::kBBytes) / unit;
   if (SW > kMaxSW) SW = kMaxSW;
 }

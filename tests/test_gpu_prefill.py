@@ -7,8 +7,8 @@ GEMM on the tensor cores) against the oracle O-PF (reading A25).
   * random fp16 tokens: every Y element against the fp64 GEMM of the decompressed weights, normwise and floored
     relative error <= 1e-4 (fp32 accumulation over N <= 2048 products), T from 1 to 300 (ragged N tiles, two
     passes), problems smaller than one CTA's share and row blocks split across CTAs;
-  * full-size Llama-3-8B shapes at the bench's T on sampled rows (bar 1e-3), determinism, the workspace's counters and
-    partial slots back at rest (canary after it), and the ABI's rejections.
+  * full-size Llama-3-8B shapes at the bench's T on sampled rows (bar 1e-3), determinism, the workspace's arrival
+    counters back at rest (canary after it), and the ABI's rejections.
 """
 import numpy as np
 import pytest
@@ -60,7 +60,7 @@ class _CanaryWs:
         Us = n_rb * (w.N // 128)
         C = min(torch.cuda.get_device_properties(0).multi_processor_count, (Us + 7) // 8)
         NT = next(v for v in (16, 32, 64, 128, 256) if min(T, 256) <= v)
-        self.rest = ((n_rb + 1) * 4 + 255) // 256 * 256 + C * 2 * NT * 128 * 4   # counters + partial slots
+        self.rest = (n_rb + 1) * 4       # the arrival counters (partial slots and token tiles: any content at rest)
 
     def ok(self):
         return bool(torch.all(self.full[self.nbytes:] == 0x5A)) and bool(torch.all(self.buf[:self.rest] == 0xFF))
