@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
       const int myslot = rb == V0 / NG ? 0 : 1;
       float* part = p.ws_part + ((size_t)cta * 2 + myslot) * (NT * 128);
       PH(3);
-      mbar_wait_sleep(&bar_dfull[db], (seg / GE::kDB) & 1);
+      mbar_wait_backoff(&bar_dfull[db], (seg / GE::kDB) & 1, 1000);   // off the critical path: poll rarely
       tc_fence_after();
       PH(0);
 #pragma unroll 1
