@@ -270,8 +270,13 @@ __global__ void __launch_bounds__(kGW * 32, kGC) gemv_group_kernel(GroupParams P
     const int xoff = gq < P.l ? gq * 4 + c : 0;
     const int xstride = P.l * 4;
     // lane (gq, c) reads word c of rows 16 i + gq and 16 i + gq + 8, i = 4 hf .. 4 hf + 3 (chunk swizzle of sbvr.h)
-    const int swz_a = chunk_swizzle(K, gq), swz_b = chunk_swizzle(K, gq + 8);
+    const int swz_a = chunk_swizzle(K, gq);         // (= chunk_swizzle(K, gq + 8) for K = 2, 3, 4)
     const int row_a = 64 * hf + gq;                 // + 16 i' (i' = 0..3), + 8 for the second row of the lane
+    // lane-constant byte offsets of word c of plane t in the lane's first row (the swizzle folded in once): every
+    // plane-word load of a unit is then slot base + lo[t] + an immediate
+    uint32_t lo[K];
+#pragma unroll
+    for (int t = 0; t < K; ++t) lo[t] = (uint32_t)(row_a * 16 * K + 4 * c + 16 * (t ^ swz_a));
 
     float2 acc[4];
 #pragma unroll
@@ -344,12 +349,11 @@ __global__ void __launch_bounds__(kGW * 32, kGC) gemv_group_kernel(GroupParams P
   #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int r = row_a + 16 * (ib + j);
-          const uint8_t* ra = sl + r * 16 * K + 4 * c;
-          const uint8_t* rb8 = ra + 8 * 16 * K;
   #pragma unroll
           for (int t = 0; t < K; ++t) {
-            w[j][2 * t] = *reinterpret_cast<const uint32_t*>(ra + 16 * (t ^ swz_a));
-            w[j][2 * t + 1] = *reinterpret_cast<const uint32_t*>(rb8 + 16 * (t ^ swz_b));
+            const uint8_t* pa = sl + lo[t] + 16 * (ib + j) * 16 * K;
+            w[j][2 * t] = *reinterpret_cast<const uint32_t*>(pa);
+            w[j][2 * t + 1] = *reinterpret_cast<const uint32_t*>(pa + 8 * 16 * K);
           }
           sb0[j] = *reinterpret_cast<const uint32_t*>(sl + UG::kSb + 4 * r);
           sb1[j] = *reinterpret_cast<const uint32_t*>(sl + UG::kSb + 4 * (r + 8));
