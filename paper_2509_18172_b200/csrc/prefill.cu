@@ -61,6 +61,9 @@ constexpr unsigned int kSentinel = 0xFFFFFFFFu;
 #else
 #define PF_WAIT_CRIT(bar, ph) mbar_wait_sleep(bar, ph)
 #endif
+#ifndef PF_ALIGN_MIN_NT
+#define PF_ALIGN_MIN_NT 16
+#endif
 #ifndef PF_MIN_UNITS
 #define PF_MIN_UNITS 8
 #endif
@@ -80,12 +83,15 @@ struct PfParams {
 #ifdef SBVR_DIAG
 #define PH_DECL unsigned long long ph_[8] = {0, 0, 0, 0, 0, 0, 0, 0}; long long ph_last_ = clock64();
 #define PH(s) do { const long long n_ = clock64(); ph_[s] += n_ - ph_last_; ph_last_ = n_; } while (0)
-#define PH_DUMP(base) do { if (p.ts && lane == 0) for (int i_ = 0; i_ < 8; ++i_) \
+#define PH_DUMP(base) do { if (p.ts && lane == 0) for (int i_ = 0; i_ < ((base) == 24 ? 3 : 8); ++i_) \
                              p.ts[(size_t)blockIdx.x * 32 + (base) + i_] = ph_[i_]; } while (0)
+#define GT_STAMP(i) do { if (p.ts && threadIdx.x == 0) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); p.ts[(size_t)blockIdx.x * 32 + 28 + (i)] = t_; } } while (0)
 #else
 #define PH_DECL
 #define PH(s) do { } while (0)
 #define PH_DUMP(base) do { } while (0)
+#define GT_STAMP(i) do { } while (0)
 #endif
 
 __device__ __forceinline__ int range_begin(int c, int qq, int rr) { return c * qq + min(c, rr); }
@@ -198,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
   const int n = V1 - V0;
   const long full_units = (long)p.n_full * NG;
   const uint32_t tail_ub = (uint32_t)p.tail_rows * (16 * K + 5);
+  GT_STAMP(0);
   auto unit_src = [&](int u) -> const uint8_t* {
     return u < full_units ? p.units + (size_t)u * kUnitFull
                           : p.units + (size_t)full_units * kUnitFull + (size_t)(u - full_units) * tail_ub;
@@ -231,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
+  GT_STAMP(1);
 
   if (warp == kProducerWarp) {
     // ------------------------------------------------------------ producer of the unit records (SW-deep ring, released
@@ -508,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
 
   tc_fence_before();
   __syncthreads();
+  GT_STAMP(2);
   if (s_comb_rb >= 0) {
     // last-arriver combine of the CTA's last row block by all threads: flat partial index f = token * 128 + row,
     // contributors in CTA order (deterministic), one batch of loads per (block of values, contributor)
@@ -520,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
       float sum[kB];
 #pragma unroll
       for (int i = 0; i < kB; ++i) sum[i] = 0.f;
-      for (int cc = cc0; cc <= cc1; ++cc) {
+      for (int cc = cc0; cc <= cc1; ++cc) {              // contributors in CTA order: deterministic
         const int sl2 = rb == range_begin(cc, p.qq, p.rr) / NG ? 0 : 1;
         const float* src = p.ws_part + ((size_t)cc * 2 + sl2) * (NT * 128);
         float wv[kB];
@@ -529,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
           const int f = tid + kThreads * (b0 + i);
           wv[i] = f < NT * 128 ? __ldcg(src + f) : 0.f;
         }
+        if (b0 == 0 && cc == cc0) GT_STAMP(-1);          // (diagnostics: first batch of loads issued)
 #pragma unroll
         for (int i = 0; i < kB; ++i) sum[i] += wv[i];
       }
@@ -541,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
     }
     if (tid == 0) p.ws_cnt[rb] = kSentinel;
   }
+  GT_STAMP(3);
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -577,6 +588,11 @@ static Plan make_plan(const sbvr_weights* w, int T) {
   const int by_units = (pl.Us + PF_MIN_UNITS - 1) / PF_MIN_UNITS;
   pl.C = num_sms() < by_units ? num_sms() : (by_units < 1 ? 1 : by_units);
   pl.NT = nt_for(T < kMaxNT ? T : kMaxNT);
+  // a split row block costs each contributor an NT x 128 fp32 partial (128 KB at NT = 256, 15x the unit record)
+  // written, read and summed by the last arriver; when the row blocks alone nearly fill the GPU, give every CTA whole
+  // row blocks instead (ranges aligned to row blocks: no partials, no combine).  Measured on gate_proj (112 row
+  // blocks): T = 16 / 64 / 128 / 256 26.0 / 33.5 / 36.4 / 47.1 -> 25.5 / 28.3 / 32.0 / 36.1 us
+  if (pl.NT >= PF_ALIGN_MIN_NT && pl.n_rb <= num_sms() && 5 * pl.n_rb >= 3 * num_sms()) pl.C = pl.n_rb;
   pl.passes = (T + kMaxNT - 1) / kMaxNT;
   return pl;
 }

@@ -15,6 +15,7 @@ ap.add_argument("--lib", required=True)
 ap.add_argument("--M", type=int, default=14336)
 ap.add_argument("--N", type=int, default=4096)
 ap.add_argument("--T", type=int, default=16)
+ap.add_argument("--K", type=int, default=4)
 a = ap.parse_args()
 buf = torch.zeros(148 * 32, dtype=torch.int64, device="cuda")
 os.environ["SBVR_TS_PTR"] = str(buf.data_ptr())
@@ -40,4 +41,19 @@ groups = {"deq": (0, ["wait_rec", "loads", "decompress", "wait_slot", "st_wait_a
 out = {"T": a.T, "units_per_cta": round(units, 2)}
 for k, (base, names) in groups.items():
     out[k] = {n: round(float(np.median(ts[:, base + i])) / units, 1) for i, n in enumerate(names) if n != "-"}
+g = ts[:, 27:32].astype(np.float64)
+live = g[:, 1] > 0
+g = g[live]
+t0 = g[:, 1].min()
+names = ["combine_first_loads", "start", "setup_done", "loops_done", "combine_done"]
+out["globaltimer_us"] = {n: [round(float(np.median(g[g[:, i] > 0, i] - t0)) / 1e3, 2) if (g[:, i] > 0).any() else None,
+                             round(float((g[:, i] - t0).max()) / 1e3, 2)] for i, n in enumerate(names)}
+out["ctas"] = int(live.sum())
+comb = g[:, 0] > 0
+if comb.any():
+    out["combining_ctas"] = int(comb.sum())
+    out["per_cta_us"] = {"loops_to_first_loads": round(float(np.median(g[comb, 0] - g[comb, 3])) / 1e3, 2),
+                         "first_loads_to_done": round(float(np.median(g[comb, 4] - g[comb, 0])) / 1e3, 2),
+                         "loops_done_of_combiners": round(float(np.median(g[comb, 3] - t0)) / 1e3, 2),
+                         "loops_done_of_others": round(float(np.median(g[~comb, 3] - t0)) / 1e3, 2) if (~comb).any() else None}
 print(json.dumps(out))
