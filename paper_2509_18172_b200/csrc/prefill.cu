@@ -51,7 +51,7 @@ constexpr int kMaxPlanes = 4;
 constexpr int kSmemBudget = 220 * 1024;
 constexpr unsigned int kSentinel = 0xFFFFFFFFu;
 #ifndef PF_ABL
-#define PF_ABL 0   // ablation bits (diagnostic builds only): 1 no decompression arithmetic, 2 no MMAs
+#define PF_ABL 0   // ablation bits (diagnostic builds only): 1 no decompression arithmetic, 2 no MMAs, 4 no tail-combine loads
 #endif
 #ifndef PF_SPIN
 #define PF_SPIN 0   // 1: the critical-path waits (records, A slots, token tiles) spin instead of suspending
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
 #pragma unroll
         for (int i = 0; i < kB; ++i) {
           const int f = tid + kThreads * (b0 + i);
-          wv[i] = f < NT * 128 ? __ldcg(src + f) : 0.f;
+          wv[i] = (f < NT * 128 && !(PF_ABL & 4)) ? __ldcg(src + f) : 0.f;
         }
         if (b0 == 0 && cc == cc0) GT_STAMP(-1);          // (diagnostics: first batch of loads issued)
 #pragma unroll
