@@ -1,14 +1,16 @@
 /*
  * sbvr.h -- C-ABI of libsbvr: the SBVR (arXiv 2509.18172) hot path on NVIDIA B200 (sm_100a).
  *
- * The four calls follow the paper's problem statement: encode
+ * The core calls follow the paper's problem statement: encode
  * weights offline, convert activations online, and run the GEMV directly on the SBVR
  * format without decompressing it.
  *
  *   sbvr_encode_weights   Section 4.2, Eq. 4-11, Algorithm 1, bit assignment
  *   sbvr_encode_vector    Section 4.3, Eq. 12
  *   sbvr_gemv             Section 4.4: y = W x on SBVR weights, x either fp16 or SBVR
- *   sbvr_gemv_batched     the same for T <= 16 activation vectors sharing one weight fetch
+ *   sbvr_gemv_batched     the same for T <= 256 activation vectors sharing weight fetches
+ *   sbvr_gemv_group       several independent batch-1 GEMVs (a decoder layer's projections) in one launch
+ *   sbvr_prefill          Section 5.1: the prefill GEMM on FP16-decompressed weights (tensor cores)
  *
  * Conventions (all calls):
  *  - Plain C types only.  "Device" pointers are CUDA global-memory pointers on the current
