@@ -159,3 +159,15 @@ def test_prefill_rejections_and_empty():
     with pytest.raises(sb.SbvrError) as e:
         sb.prefill(w, torch.zeros(2, 256, dtype=torch.float16, device=DEV), ws=sb.Workspace(256))
     assert e.value.status == sb.ERR_WORKSPACE
+
+
+@pytest.mark.parametrize("M,N", [(16, 128), (48, 128), (16, 1024), (144, 256)])
+@pytest.mark.parametrize("T", [1, 3, 17])
+def test_prefill_tiny_shapes(M, N, T):
+    """Degenerate sizes: a single 16-row tail block, one group per row (every unit its own row block), a row block
+    smaller than one CTA's share, ragged token counts."""
+    w, enc = _make(M, N, 4, seed=700 + M + N + T)
+    X = synthetic.activation(N, seed=701 + T, T=T)
+    Y = sb.prefill(w, torch.from_numpy(X).to(DEV))
+    torch.cuda.synchronize()
+    _close(Y.cpu().numpy(), oracle.prefill_rows(enc, X))
