@@ -342,7 +342,7 @@ def run_sbvr(args, world, rank, local_rank, pg):
     # A decode step of a whole model is one CUDA graph: the timed graphs hold SPG consecutive steps (one
     # per ring layer, chained by programmatic dependent launch like the layers of a model); single-step graphs
     # serve a remainder of K that SPG does not divide.
-    spg = ring
+    spg = max(1, min(args.steps_per_graph, args.steps))     # (a run of K < SPG steps is one K-step graph)
     ev_graphs, plain_graphs, split_graphs = [], [], []
     with torch.cuda.stream(stream):
         for _ in range(3):
@@ -356,13 +356,13 @@ def run_sbvr(args, world, rank, local_rank, pg):
         multi_graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(multi_graph, stream=stream):
             for r in range(spg):
-                step(r)
+                step(r % ring)
         for gi in range(n_ev_graphs):
             span = (cr.event(), cr.event())
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
                 for r in range(spg):
-                    step(r, span=span if r == 1 % spg else None)
+                    step(r % ring, span=span if r == 1 % spg else None)
             ev_graphs.append((g, span, 0))
         for r in range(ring):
             evs = [(cr.event(), cr.event()) for _ in FUSED]
@@ -386,7 +386,7 @@ def run_sbvr(args, world, rank, local_rank, pg):
         if e2e_pipelined:
             xh_e2e = [xs_host[0].clone().pin_memory() for _ in range(spg)]
             xd_e2e = [torch.empty_like(xs[0]) for _ in range(spg)]
-            yh_e2e = [torch.zeros(yall[r].numel(), dtype=torch.float32).pin_memory() for r in range(spg)]
+            yh_e2e = [torch.zeros(yall[r % ring].numel(), dtype=torch.float32).pin_memory() for r in range(spg)]
             xd_e2e[0].copy_(xh_e2e[0])
             side = torch.cuda.Stream(device)
             evx = [torch.cuda.Event() for _ in range(spg)]
@@ -397,19 +397,19 @@ def run_sbvr(args, world, rank, local_rank, pg):
                 for r in range(spg):
                     if r > 0:
                         stream.wait_event(evx[r])
-                    step(r, xsrc=xd_e2e[r])
+                    step(r % ring, xsrc=xd_e2e[r])
                     evg[r].record(stream)
                     with torch.cuda.stream(side):
                         nr = (r + 1) % spg                 # the next step's input (r = last: the next replay's first)
                         xd_e2e[nr].copy_(xh_e2e[nr], non_blocking=True)
                         evx[nr].record(side)
                         side.wait_event(evg[r])
-                        yh_e2e[r].copy_(yall[r], non_blocking=True)
+                        yh_e2e[r].copy_(yall[r % ring], non_blocking=True)
                 stream.wait_stream(side)
         else:
             with torch.cuda.graph(e2e_multi, stream=stream):
                 for r in range(spg):
-                    step(r, e2e=True)
+                    step(r % ring, e2e=True)
     torch.cuda.synchronize()
 
     # --- algorithmic bytes (whole job: full matrices, all ranks together)
@@ -560,20 +560,21 @@ def cublas_fp16_baseline(args, device, ring=2, steps=200):
             with torch.cuda.graph(gr, stream=stream):
                 step(r)
             graphs.append(gr)
+        spg = max(1, min(args.steps_per_graph, steps))
         multi = torch.cuda.CUDAGraph()                 # as the SBVR step: consecutive steps in one graph
         with torch.cuda.graph(multi, stream=stream):
-            for r in range(ring):
-                step(r)
+            for r in range(spg):
+                step(r % ring)
         for i in range(20):
             multi.replay()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        for s in range(steps // ring):
+        for s in range(steps // spg):
             multi.replay()
         b.record(stream)
         torch.cuda.synchronize()
-    ms = a.elapsed_time(b) / (steps // ring * ring)
+    ms = a.elapsed_time(b) / (steps // spg * spg)
     byts = sum(2 * M * N + 2 * N + 2 * M for (_, M, N, _) in shapes)
     del Ws
     torch.cuda.empty_cache()
@@ -994,6 +995,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="sbvr", choices=["sbvr", "reference"])
     ap.add_argument("--ring", type=int, default=4)
+    ap.add_argument("--steps-per-graph", type=int, default=32,
+                    help="consecutive steps per timed CUDA graph: Llama-3-8B's 32 decoder layers form one decode graph "
+                         "(P:447); the layers cycle through the --ring distinct weight sets")
     ap.add_argument("--fused-conversion", action="store_true",
                     help="no sbvr_encode_vector launch: every GEMV converts its fp16 input in its prologue "
                          "(SBVR_ACT_FP16_Q, bit-identical)")
@@ -1126,6 +1130,7 @@ def main():
                    "projections": [f"{n} {M}x{N}" for n, M, N in shapes],
                    "gemvs_per_step": [f"{n} {M}x{N} = {'+'.join(m)}" for n, M, N, _, m in FUSED],
                    "K": K_BITS, "l": L_BITS, "group": G, "batch": 1, "ring_layers": args.ring,
+                   "steps_per_graph": args.steps_per_graph,
                    "l2": "inputs larger than L2: ring of 4 distinct layer weight sets (468 MB) cycled every step",
                    "parallelism": f"row-sharded over {world} GPU(s)" + ((" + NCCL all-gather of y" if args.allgather == "nccl" else
                                                                        " + y stored to every rank by the GEMV epilogue "
@@ -1171,8 +1176,9 @@ def main():
         "clocks": res["clocks"],
         "step_us": step_stats,
         "self_check": {"ok": True, **checks},
-        "timing": f"K steps = K // {res['spg']} replays of a CUDA graph holding {res['spg']} consecutive steps (one per "
-                  "ring layer, chained by programmatic dependent launch as the layers of a model's decode graph) + K % "
+        "timing": f"K steps = K // {res['spg']} replays of a CUDA graph holding {res['spg']} consecutive steps (the "
+                  f"decoder layers of one Llama-3-8B decode graph, cycling through {args.ring} distinct weight sets > L2, "
+                  "chained by programmatic dependent launch) + K % "
                   f"{res['spg']} single-step graphs; CUDA events on the replay stream after every replay (each replay and "
                   "event runs under torch.cuda.stream(stream)); value = step algorithmic bytes x K / (last event - "
                   "first event); step_us = replay time / steps in it; barrier + synchronize on both sides; max over "
