@@ -1140,11 +1140,13 @@ def main():
                             "sbvr_gemv_group x1 over the layer set (fused qkv, o, fused gate_up, down as 4 independent "
                             "problems of one persistent launch" + ("" if args.xconv == "launch" else ", whose prologue "
                             "converts the 4 fp16 inputs to SBVR-x, Eq. 12") + "; bit-sliced "
-                            "AND/popcount on the int8 tensor pipe, mma.sync m16n8k32 u8, kernel gemv_group), one CUDA "
-                            "graph per step, programmatic dependent launch" if group else
+                            "AND/popcount on the int8 tensor pipe, mma.sync m16n8k32 u8, kernel gemv_group), "
+                            f"{args.steps_per_graph} steps (decoder layers) per CUDA graph, programmatic dependent "
+                            "launch" if group else
                             "sbvr_encode_vector x1 (the 4 layer inputs) + sbvr_gemv x4 (fused qkv, o, fused gate_up, "
                             "down; bit-sliced AND/popcount on the int8 tensor pipe, mma.sync m16n8k32 u8, kernel "
-                            "gemv_mma), one CUDA graph per step, programmatic dependent launch"),
+                            f"gemv_mma), {args.steps_per_graph} steps (decoder layers) per CUDA graph, programmatic "
+                            "dependent launch"),
                    "step": args.step, "x_conversion": ("in the GEMV kernel" if (args.fused_conversion or (
                        group and args.xconv == "kernel")) else "sbvr_encode_vector launch")},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
