@@ -64,6 +64,10 @@ constexpr unsigned int kSentinel = 0xFFFFFFFFu;
 #ifndef PF_ALIGN_MIN_NT
 #define PF_ALIGN_MIN_NT 16
 #endif
+#ifndef PF_TAIL_KB
+#define PF_TAIL_KB 40   // values per thread per round of the tail combine (40: all of them at NT = 256 in one round;
+                        // measured q_proj T = 256 31.0 / 36.5 / 27.8 us at 16 / 4 / 40)
+#endif
 #ifndef PF_MIN_UNITS
 #define PF_MIN_UNITS 8
 #endif
@@ -523,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(PfParams p, int SW
     const int rb = s_comb_rb, rows = rows_of(rb);
     const int cc0 = unit_cta(rb * NG, p.qq, p.rr), cc1 = unit_cta((rb + 1) * NG - 1, p.qq, p.rr);
     constexpr int kVals = (NT * 128 + kThreads - 1) / kThreads;
-    constexpr int kB = kVals < 16 ? kVals : 16;
+    constexpr int kB = kVals < PF_TAIL_KB ? kVals : PF_TAIL_KB;
 #pragma unroll 1
     for (int b0 = 0; b0 < kVals; b0 += kB) {
       float sum[kB];
